@@ -185,9 +185,15 @@ class Query:
         return f"Query({self.name!r}, n={self.n}, m={len(self.edges)})"
 
 
-def random_query(offs, nbrs, labels, size: int, seed: int, max_restarts: int = 1000) -> Query:
+def random_query(offs, nbrs, labels, size: int, seed: int, max_restarts: int = 1000,
+                 dense: bool = False, min_avg_degree: float = 0.0) -> Query:
     """§6.1 procedure: random seed vertex, repeatedly add a uniformly random vertex
-    adjacent to the current set, keep ALL edges among chosen vertices (induced)."""
+    adjacent to the current set, keep ALL edges among chosen vertices (induced).
+
+    dense=True draws the next vertex uniformly among the frontier vertices with the MOST
+    neighbours in the chosen set (on sparse power-law graphs the plain procedure almost
+    always returns trees; Appendix A's "dense" class needs d_avg >= 3).  Restarts until
+    the query's average degree reaches min_avg_degree."""
     n = len(offs) - 1
     ctr = 0
     for _ in range(max_restarts):
@@ -196,18 +202,28 @@ def random_query(offs, nbrs, labels, size: int, seed: int, max_restarts: int = 1
         chosen = [v0]
         cset = {v0}
         while len(chosen) < size:
-            frontier = set()
+            conn = {}
             for v in chosen:
-                frontier.update(int(w) for w in nbrs[offs[v]:offs[v + 1]])
-            frontier -= cset
-            if not frontier:
+                for w in nbrs[int(offs[v]):int(offs[v + 1])]:
+                    w = int(w)
+                    if w not in cset:
+                        conn[w] = conn.get(w, 0) + 1
+            if not conn:
                 break
-            fr = sorted(frontier)
+            if dense:
+                best = max(conn.values())
+                fr = sorted(w for w, c in conn.items() if c == best)
+            else:
+                fr = sorted(conn)
             r = int(rng_u64(seed, STREAM_QUERY, ctr)); ctr += 1
             w = fr[r % len(fr)]
             chosen.append(w)
             cset.add(w)
         if len(chosen) == size:
+            idx = {v: i for i, v in enumerate(chosen)}
+            m = sum(1 for v in chosen for w in nbrs[int(offs[v]):int(offs[v + 1])] if int(w) in idx) // 2
+            if 2.0 * m / size < min_avg_degree:
+                continue
             idx = {v: i for i, v in enumerate(chosen)}
             edges = []
             for v in chosen:

@@ -1,0 +1,212 @@
+/*
+ * gmatch.h -- C ABI of the B200-native fine-grained subgraph matcher.
+ *
+ * The operations follow the problem statement of PAPER.md (gMatch, arXiv 2604.10601):
+ *   "Given a query graph Q and a data graph G, subgraph matching aims to find all
+ *    embeddings of Q in G" (§1, line 82); an embedding is an injective, label- and
+ *    edge-preserving map V(Q) -> V(G) (§2.1, Definition 1).
+ * The search itself is the paper's fine-grained DFS extension with warp-level batch
+ * exploration (§4.1-4.2, Algorithm 2) and its two-phase load balancing
+ * (initial BFS pool of tau partial matches + idle-warp work stealing, §4.3, lines
+ * 431-445), re-designed for sm_100a.
+ *
+ * Conventions for every entry point:
+ *   - Return value: GM_OK (0) on success, a positive GM_* code otherwise; a one-line
+ *     human-readable reason is then available from gm_last_error() (thread-local).
+ *     No entry point aborts the process or prints.
+ *   - `mem` arguments say where a caller buffer lives: GM_MEM_HOST (pageable or
+ *     pinned host memory) or GM_MEM_DEVICE (memory of the current CUDA device).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls may synchronize `stream` internally where the host needs a device value
+ *     (pool sizes, candidate counts); they return only after results are visible in
+ *     the caller's output buffers.
+ *   - Opaque handles (gm_graph, gm_plan) own device memory on the device that was
+ *     current at creation; free them with gm_free_graph / gm_free_plan.  A plan
+ *     borrows its graph: free plans before their graph.
+ *   - Vertex ids are uint32 in [0, n); labels are uint32 in [0, num_labels).
+ *   - Limits: n * num_labels < 2^32, stored adjacency entries < 2^32,
+ *     query size 1 <= nq <= GM_MAX_QUERY.  Exceeding a limit returns GM_ERR_LIMIT.
+ */
+#ifndef GMATCH_H
+#define GMATCH_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GM_API __attribute__((visibility("default")))
+#else
+#define GM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GM_OK            0
+#define GM_ERR_ARG       1   /* invalid argument (null pointer, bad id, disconnected query...) */
+#define GM_ERR_CUDA      2   /* a CUDA runtime call failed */
+#define GM_ERR_NOMEM     3   /* device allocation failed */
+#define GM_ERR_LIMIT     4   /* a size limit documented above was exceeded */
+#define GM_TIMEOUT       5   /* time limit hit: the reported count is a lower bound */
+
+#define GM_MEM_HOST      0
+#define GM_MEM_DEVICE    1
+
+#define GM_MAX_QUERY     32
+
+/* candidate filters (gm_plan_query `filter`) */
+#define GM_FILTER_NONE   0   /* label only */
+#define GM_FILTER_LDF    1   /* label and degree: L(v)=L(u), d(v) >= d(u) */
+#define GM_FILTER_NLF    2   /* LDF + neighbour label frequency: for all labels l,
+                                |N(v) with label l| >= |N(u) with label l| */
+
+typedef struct gm_graph gm_graph;
+typedef struct gm_plan gm_plan;
+
+/* ------------------------------------------------------------------ graph */
+
+/*
+ * gm_load_graph -- build the device data graph G from an edge list.
+ *   n            number of vertices.
+ *   m            number of (src[i], dst[i]) pairs.  Pairs are undirected edges;
+ *                self loops and repeated pairs are dropped (G is simple, as
+ *                Definition 1 assumes).
+ *   src, dst     m vertex ids each, in `mem`.  Read only; not retained.
+ *   labels       n labels in `mem`, or NULL for an unlabelled graph (all label 0).
+ *   num_labels   |Sigma| >= 1; every label must be < num_labels.
+ * Layout built: row r = v*num_labels + l holds
+ * the neighbours of v whose label is l, ascending; offs has n*num_labels+1 entries.
+ * On success *out receives a handle.  Needs ~40 bytes of scratch per input pair.
+ */
+GM_API int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const uint32_t *dst,
+                  const uint32_t *labels, uint32_t num_labels, int mem, void *stream,
+                  gm_graph **out);
+
+typedef struct {
+    uint64_t n;            /* vertices */
+    uint64_t num_adj;      /* stored adjacency entries = 2 |E(G)| */
+    uint32_t num_labels;
+    uint32_t d_max;        /* maximum degree */
+    uint64_t device_bytes; /* device memory held by the graph */
+} gm_graph_info_t;
+
+GM_API int gm_graph_info(const gm_graph *g, gm_graph_info_t *info);
+
+/*
+ * gm_graph_export -- copy the CSR back to host buffers (tests, debugging).
+ *   offs_host: n*num_labels+1 uint32; nbr_host: num_adj uint32; labels_host: n uint32.
+ *   Any pointer may be NULL to skip that array.
+ */
+GM_API int gm_graph_export(const gm_graph *g, uint32_t *offs_host, uint32_t *nbr_host, uint32_t *labels_host);
+
+GM_API void gm_free_graph(gm_graph *g);
+
+/* ------------------------------------------------------------------ query plan */
+
+/*
+ * gm_plan_query -- prepare query Q against G: candidate filter, matching order.
+ *   nq, mq       |V(Q)| (1..GM_MAX_QUERY) and number of query edges.
+ *   qedges       2*mq host uint32: edge i joins qedges[2i] and qedges[2i+1].
+ *   qlabels      nq host uint32 labels.
+ *   order        NULL for the planner's order (RI-style greedy, §3:
+ *                "we generate phi on the CPU using the RI method"), or nq host uint32
+ *                giving phi[0..nq-1]; it must be a permutation whose every vertex after
+ *                the first has an earlier neighbour ("connected", §2.2),
+ *                else GM_ERR_ARG.
+ *   filter       GM_FILTER_NONE / _LDF / _NLF; every filter is sound (it never removes
+ *                the image of a query vertex under an embedding), so counts do not
+ *                depend on it.
+ * Q must be connected (GM_ERR_ARG otherwise).  Runs the filter kernel on `stream`
+ * and synchronizes it (the order uses the candidate counts).
+ */
+GM_API int gm_plan_query(const gm_graph *g, uint32_t nq, uint32_t mq, const uint32_t *qedges,
+                  const uint32_t *qlabels, const uint32_t *order, uint32_t filter,
+                  void *stream, gm_plan **out);
+
+typedef struct {
+    uint32_t nq;
+    uint32_t order[GM_MAX_QUERY];       /* phi */
+    uint32_t backward[GM_MAX_QUERY];    /* bit i of backward[l]: phi[i] is a backward
+                                           neighbour of phi[l] (N_+^phi, Table 1) */
+    uint64_t cand_count[GM_MAX_QUERY];  /* |C(u)| after filtering, by query vertex id */
+} gm_plan_info_t;
+
+GM_API int gm_plan_info(const gm_plan *p, gm_plan_info_t *info);
+
+/*
+ * gm_plan_candidates -- copy the candidate bitmap of query vertex u to the host:
+ * bit (v % 32) of word v / 32 is 1 iff v passed the filter for u.  words_host holds
+ * ceil(n/32) uint32.
+ */
+GM_API int gm_plan_candidates(const gm_plan *p, uint32_t u, uint32_t *words_host);
+
+GM_API void gm_free_plan(gm_plan *p);
+
+/* ------------------------------------------------------------------ search */
+
+typedef struct {
+    uint64_t tau;            /* initial task-pool threshold (§4.3); 0 = 1e6 */
+    uint32_t rank, world;    /* this rank's share of the root candidates: vertex v is
+                                owned by rank (v / root_chunk) % world; world 0 = 1 */
+    uint32_t root_chunk;     /* 0 = 64 */
+    uint32_t steal;          /* 1 = idle-warp work stealing on (gm_default_opts), 0 = off */
+    uint32_t blocks_per_sm;  /* 0 = as many as fit */
+    uint32_t warps_per_block;/* 0 = 4 */
+    double   time_limit_ms;  /* 0 = none; on expiry the call returns GM_TIMEOUT */
+    const uint32_t *roots;   /* optional host list restricting phi[0]'s images to
+                                these vertices (still filtered and rank-partitioned) */
+    uint64_t num_roots;
+    uint64_t pool_bytes_max; /* cap on the BFS pool's device bytes; 0 = 1 GiB */
+} gm_run_opts;
+
+GM_API void gm_default_opts(gm_run_opts *o);
+
+typedef struct {
+    uint64_t count;           /* embeddings found by this rank */
+    uint64_t roots;           /* root candidates owned by this rank */
+    uint64_t pool_size;       /* partial matches in the initial pool */
+    uint32_t pool_depth;      /* their length */
+    uint32_t timed_out;
+    uint64_t donations;       /* work items handed to idle warps (stealing) */
+    uint64_t tasks;           /* candidate checks T_M(u,v) performed by the DFS kernel */
+    uint64_t rounds;          /* warp scatter rounds (32-wide task batches) */
+    float    dfs_ms;          /* device time of the DFS kernel launch (CUDA events) */
+    float    total_ms;        /* device time of the whole call on `stream` */
+    uint32_t dfs_launches;    /* DFS kernel launches in this call (0 or 1) */
+    uint32_t kernel_launches; /* all kernels this call launched */
+    uint32_t grid, block;     /* DFS launch shape */
+    uint64_t words;           /* 4-byte words the DFS kernel read from the CSR and the candidate
+                                 bitmaps: candidate reads + row-offset pairs + binary-search
+                                 probes + bitmap words (algorithmic bytes = 4 * words) */
+} gm_run_stats;
+
+/*
+ * gm_count -- count all embeddings of the plan's Q in G (this rank's share).
+ *   count_out   one uint64 in `mem` receiving the count (device memory lets the
+ *               caller all-reduce it across ranks without a host round trip).
+ *   stats       optional host struct.
+ * Returns GM_OK, or GM_TIMEOUT (count is the number found before the limit).
+ */
+GM_API int gm_count(const gm_plan *p, const gm_run_opts *opts, uint64_t *count_out, int mem,
+             gm_run_stats *stats, void *stream);
+
+/*
+ * gm_enumerate -- list embeddings: row k of `out` (nq uint32, in `mem`) holds the data
+ * vertex of query vertex u at column u.  At most `capacity` rows are written, in no
+ * particular order; *count_host receives the total number of embeddings (which may
+ * exceed capacity: rows past capacity are counted but not written).
+ */
+GM_API int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t *out, uint64_t capacity,
+                 int mem, uint64_t *count_host, gm_run_stats *stats, void *stream);
+
+/* Thread-local description of the last error (empty string if none). */
+GM_API const char *gm_last_error(void);
+
+/* Library version string. */
+GM_API const char *gm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GMATCH_H */

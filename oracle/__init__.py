@@ -43,6 +43,8 @@ def _load():
         lib.or_count.restype = ctypes.c_uint64
         lib.or_count.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, _u32p,
                                  ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, _u32p, ctypes.c_uint64]
+        lib.or_count_budget.restype = ctypes.c_uint64
+        lib.or_count_budget.argtypes = lib.or_count.argtypes + [ctypes.c_uint64]
         lib.or_filter.restype = ctypes.c_int
         lib.or_filter.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, _u32p,
                                   ctypes.c_int, ctypes.c_uint32, _u8p]
@@ -79,15 +81,19 @@ class OracleGraph:
         lib.or_graph_export(self._h, _p(off, _i64p), _p(adj))
         return off, adj[:m2]
 
-    def count(self, q, fixed=None, limit=0) -> int:
-        """Number of embeddings of q (Definition 1); fixed=(u, v) pins M[u] = v."""
+    def count(self, q, fixed=None, limit=0, max_nodes=0):
+        """Number of embeddings of q (Definition 1); fixed=(u, v) pins M[u] = v.
+        With max_nodes > 0 returns None when the search needs more tree nodes than that."""
         lib = _load()
         qe = np.ascontiguousarray(q.edges, dtype=np.uint32).reshape(-1)
         ql = np.ascontiguousarray(q.labels, dtype=np.uint32)
         fu, fv = (-1, 0) if fixed is None else (int(fixed[0]), int(fixed[1]))
-        r = lib.or_count(self._h, q.n, len(q.edges), _p(qe), _p(ql), fu, fv, limit, None, 0)
+        r = lib.or_count_budget(self._h, q.n, len(q.edges), _p(qe), _p(ql), fu, fv, limit, None, 0,
+                                int(max_nodes))
         if r == 2 ** 64 - 1:
             raise ValueError("oracle: bad query")
+        if r == 2 ** 64 - 2:
+            return None
         return int(r)
 
     def enumerate(self, q, fixed=None, cap=None) -> np.ndarray:

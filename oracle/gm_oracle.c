@@ -111,6 +111,7 @@ typedef struct {
     uint32_t map[64];          /* map[u] = data vertex of query vertex u */
     uint8_t *used;             /* used[v] = 1 if v is the image of some query vertex */
     uint64_t count, limit;
+    uint64_t nodes, max_nodes;  /* search-tree nodes visited; budget (0 = none) */
     uint32_t *out;
     uint64_t out_cap;
     int fixed_u;
@@ -136,6 +137,7 @@ static void emit(or_ctx *c) {
 
 static void search(or_ctx *c, int depth) {
     if (c->limit && c->count >= c->limit) return;
+    if (c->max_nodes && ++c->nodes > c->max_nodes) return;   /* budget exhausted: caller discards */
     if (depth == c->nq) { emit(c); return; }
     int u = c->order[depth];
     if (depth == 0 && c->fixed_u >= 0) {
@@ -174,13 +176,28 @@ static void search(or_ctx *c, int depth) {
  *   out_cap embeddings, each nq data-vertex ids indexed by query vertex id.
  * Returns the number of embeddings found (-1 on bad arguments, as UINT64_MAX).
  */
+uint64_t or_count_budget(const or_graph *g, int nq, int mq, const uint32_t *qedges,
+                         const uint32_t *qlabels, int fixed_u, uint32_t fixed_v, uint64_t limit,
+                         uint32_t *out, uint64_t out_cap, uint64_t max_nodes);
+
 uint64_t or_count(const or_graph *g, int nq, int mq, const uint32_t *qedges,
                   const uint32_t *qlabels, int fixed_u, uint32_t fixed_v, uint64_t limit,
                   uint32_t *out, uint64_t out_cap) {
+    return or_count_budget(g, nq, mq, qedges, qlabels, fixed_u, fixed_v, limit, out, out_cap, 0);
+}
+
+/*
+ * Same as or_count, with a budget of max_nodes visited search-tree nodes (0 = none).
+ * Returns UINT64_MAX - 1 when the budget ran out (the count is then unknown); used only to
+ * pick samples the oracle can finish, never to produce a partial expected value.
+ */
+uint64_t or_count_budget(const or_graph *g, int nq, int mq, const uint32_t *qedges,
+                         const uint32_t *qlabels, int fixed_u, uint32_t fixed_v, uint64_t limit,
+                         uint32_t *out, uint64_t out_cap, uint64_t max_nodes) {
     if (nq <= 0 || nq > 64) return UINT64_MAX;
     or_ctx *c = (or_ctx *)calloc(1, sizeof(or_ctx));
     c->g = g; c->nq = nq; c->qlab = qlabels; c->limit = limit; c->out = out; c->out_cap = out_cap;
-    c->fixed_u = fixed_u; c->fixed_v = fixed_v;
+    c->fixed_u = fixed_u; c->fixed_v = fixed_v; c->max_nodes = max_nodes;
     for (int i = 0; i < mq; i++) {
         uint32_t a = qedges[2 * i], b = qedges[2 * i + 1];
         if (a >= (uint32_t)nq || b >= (uint32_t)nq) { free(c); return UINT64_MAX; }
@@ -205,7 +222,7 @@ uint64_t or_count(const or_graph *g, int nq, int mq, const uint32_t *qedges,
     }
     c->used = (uint8_t *)calloc((size_t)g->n + 1, 1);
     search(c, 0);
-    uint64_t r = c->count;
+    uint64_t r = (c->max_nodes && c->nodes > c->max_nodes) ? UINT64_MAX - 1 : c->count;
     free(c->used); free(c);
     return r;
 }

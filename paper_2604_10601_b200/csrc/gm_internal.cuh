@@ -1,0 +1,65 @@
+// gm_internal.cuh -- shared internals of libgmatch (graph/plan structs, error plumbing).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/gmatch.h"
+
+namespace gm {
+
+void set_error(const char *fmt, ...);
+
+#define GM_CK(call)                                                                   \
+    do {                                                                              \
+        cudaError_t _e = (call);                                                      \
+        if (_e != cudaSuccess) {                                                      \
+            ::gm::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,                \
+                            cudaGetErrorString(_e));                                  \
+            return _e == cudaErrorMemoryAllocation ? GM_ERR_NOMEM : GM_ERR_CUDA;      \
+        }                                                                             \
+    } while (0)
+
+#define GM_REQ(cond, code, ...)                                                       \
+    do {                                                                              \
+        if (!(cond)) {                                                                \
+            ::gm::set_error(__VA_ARGS__);                                             \
+            return (code);                                                            \
+        }                                                                             \
+    } while (0)
+
+constexpr int kWarp = 32;
+constexpr int kMaxQ = GM_MAX_QUERY;
+
+}  // namespace gm
+
+// Device data graph: label-partitioned CSR.
+struct gm_graph {
+    uint64_t n = 0;
+    uint32_t S = 1;            // number of labels
+    uint64_t nadj = 0;         // stored adjacency entries
+    uint32_t dmax = 0;
+    int device = 0;
+    uint32_t *offs = nullptr;  // n*S + 1 row offsets (row = v*S + label)
+    uint32_t *nbr = nullptr;   // nadj neighbour ids, ascending inside each row
+    uint32_t *lab = nullptr;   // n vertex labels
+    uint64_t bytes = 0;
+};
+
+// Query plan: matching order, backward sets, candidate bitmaps.
+struct gm_plan {
+    const gm_graph *g = nullptr;
+    uint32_t nq = 0;
+    uint32_t order[gm::kMaxQ];      // phi[l] = query vertex at position l
+    uint32_t pos[gm::kMaxQ];        // inverse of order
+    uint32_t qlab[gm::kMaxQ];       // label by query vertex id
+    uint32_t qdeg[gm::kMaxQ];
+    uint32_t qadj[gm::kMaxQ];       // adjacency bitmask by query vertex id
+    uint32_t bw[gm::kMaxQ];         // bit i of bw[l]: phi[i] adjacent to phi[l], i < l
+    uint64_t cand_count[gm::kMaxQ]; // by query vertex id
+    uint32_t filter = 0;
+    uint32_t words = 0;             // ceil(n/32)
+    uint32_t *cand = nullptr;       // nq * words bitmaps, by query vertex id
+};

@@ -1,0 +1,864 @@
+// search.cu -- gm_count / gm_enumerate: the fine-grained DFS extension of partial matches.
+//
+// PAPER.md §4-§5 (lines 362-544) re-designed for sm_100a:
+//
+//  * Initialization phase (§4.3; Alg. 2 line 1): breadth-first expansion of
+//    the root candidates level by level (k_expand, one warp per partial match, count pass
+//    then write pass) until the pool holds >= tau partial matches.  The pool is stored
+//    level-major (pool[i * P + k] = M_k[phi[i]]) so a warp loads 32 pool items with
+//    coalesced 128-byte reads.
+//  * Fine-grained execution (§4.1) + warp-level batch exploration (§4.2) (k_dfs): each
+//    warp owns an execution stack S[level][lane] in shared memory (Alg. 2 §5.1: fields
+//    v, pid, and the local candidate set C, kept here as a (begin, length, source-level)
+//    slice of the label-partitioned CSR), i.e. O(|V(Q)| * 32) entries independent of
+//    d_max (§5.2).  Each round, the 32 lanes take the next 32 tasks T_M(u, v) from the
+//    virtual task pool formed by ALL parent lanes' remaining candidate slices (the two
+//    cursors of §4.2 / ScatterTask), computed warp-parallel with a shuffle scan instead
+//    of Alg. 2's serial leader loop; every lane validates its task (candidate filter bit,
+//    injectivity and backward-neighbour adjacency by binary search, fused in one walk up
+//    the pid chain, §5.2 "We fuse these checks into a single loop"); a ballot decides
+//    whether to descend (Alg. 2 lines 15-16).
+//  * Load balancing (§4.3): warps fetch 32 pool items at a time with one atomicAdd (the
+//    pool items become the 32 lanes of the base level: batch exploration starts at the
+//    pool); an idle warp posts one steal request (global counter); a busy warp that
+//    claims a request hands off the untouched part of its shallowest splittable stack
+//    level (its last untouched parent lane, or the upper half of the current slice)
+//    through a bounded MPMC ring -- the paper's "idle warps receive half of the work
+//    from busy warps by splitting the execution stack", via a ring instead of a direct
+//    warp-to-warp hand-off.  Termination: `work` counts warps holding work plus items in
+//    the ring; a warp exits when the pool is exhausted and work == 0.
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "gm_internal.cuh"
+
+namespace gm {
+
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr uint32_t kItemWords = 4 + kMaxQ;     // [depth, cb, cl, cs, prefix[kMaxQ]]
+
+// Global control block.  Every field that many warps poll or update lives on its own
+// 128-byte line so that the pollers of one do not serialise the atomics of another.
+struct Ctrl {
+    alignas(128) unsigned long long pool_ctr;
+    alignas(128) int work;                    // warps holding work + items in the ring
+    alignas(128) int requests;                // posted steal requests not yet served
+    alignas(128) unsigned long long q_head;   // ring positions (monotone, 64-bit: never wrap)
+    alignas(128) unsigned long long q_tail;
+    alignas(128) int abort;
+    alignas(128) unsigned long long out_ctr;
+    alignas(128) unsigned long long count;
+    unsigned long long tasks;
+    unsigned long long rounds;
+    unsigned long long words;   // algorithmic 4-byte words read by k_dfs
+    unsigned long long donations;
+};
+
+struct SearchParams {
+    const uint32_t *__restrict__ offs;
+    const uint32_t *__restrict__ nbr;
+    const uint32_t *__restrict__ cand;
+    uint32_t S, nq, words, use_cand;
+    uint32_t lab[kMaxQ];        // L(phi[l])
+    uint32_t bw[kMaxQ];         // backward positions of phi[l]
+    uint32_t candoff[kMaxQ];    // word offset of phi[l]'s candidate bitmap (phi[l] * words)
+    uint32_t col[kMaxQ];        // output column of position l (= phi[l])
+    const uint32_t *pool;       // level-major, pool_size items of depth d0
+    unsigned long long pool_size;
+    uint32_t d0;
+    uint32_t steal;
+    Ctrl *ctrl;
+    uint32_t batch;             // pool items fetched per warp (<= 32)
+    uint32_t *q_items;          // q_cap * kItemWords
+    unsigned long long *q_seq;  // q_cap per-slot sequence numbers (Vyukov bounded MPMC ring)
+    unsigned long long q_cap;
+    uint32_t *out;              // enumerate rows (nq words each)
+    unsigned long long out_cap;
+    unsigned long long deadline_ns;  // 0 = no limit
+};
+
+// ------------------------------------------------------------------ device helpers
+
+__device__ __forceinline__ uint32_t ld_nc(const uint32_t *p) { return __ldg(p); }
+
+// v in sorted nbr[lo, hi)?  Branch-free lower bound; ceil(log2(hi-lo)) + 1 word reads,
+// added to `words` (the algorithmic-bytes counter).
+__device__ __forceinline__ bool contains(const uint32_t *__restrict__ nbr, uint32_t lo, uint32_t hi, uint32_t v,
+                                         uint32_t &words) {
+    uint32_t n = hi - lo;
+    if (n == 0) return false;
+    const uint32_t *base = nbr + lo;
+    while (n > 1) {
+        const uint32_t half = n >> 1;
+        base = (ld_nc(base + half) <= v) ? base + half : base;
+        n -= half;
+        ++words;
+    }
+    ++words;
+    return ld_nc(base) == v;
+}
+
+__device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint32_t v, uint32_t &words) {
+    if (!P.use_cand) return true;
+    ++words;
+    return (ld_nc(P.cand + P.candoff[l] + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int D>
+struct WarpStack {
+    uint32_t v[D][32];    // S[l][lane].v   : candidate data vertex of the task in this lane
+    uint32_t cb[D][32];   // S[l][lane].C   : begin of the local candidate slice of lane's partial match
+    uint32_t cl[D][32];   //                  its length
+    uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
+    uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
+    uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
+    uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
+};
+
+// GenerateTask (Alg. 2 lines 17-24, Erratum 2 read as a running minimum): the local
+// candidate set of the partial match ending at (l-1, lane) is the label-L(phi[l]) slice
+// of N(M[u']) for the backward neighbour u' with the fewest such neighbours (§4.1).
+template <int D>
+__device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane,
+                                         uint32_t &words) {
+    uint32_t best = 0, cb = 0, cs = 0;
+    if (valid) {
+        const uint32_t bw = P.bw[l];
+        const uint32_t lab = P.lab[l];
+        const int lowest = __ffs(bw) - 1;
+        best = 0xffffffffu;
+        uint32_t p = lane;
+        for (int i = l - 1; i >= lowest; --i) {
+            if ((bw >> i) & 1u) {
+                const uint32_t row = S.v[i][p] * P.S + lab;
+                const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
+                words += 2;
+                if (hi - lo < best) { best = hi - lo; cb = lo; cs = (uint32_t)i; }
+            }
+            p = S.pid[i][p];
+        }
+    }
+    S.cb[l][lane] = cb;
+    S.cl[l][lane] = best;
+    S.cs[l][lane] = (uint8_t)cs;
+}
+
+// Process (Alg. 2 lines 32-41, Erratum 1 read as "lanes without a task return false"):
+// candidate-filter bit, then one walk up the pid chain checking injectivity and, for each
+// backward neighbour other than the slice's source, adjacency by binary search.
+template <int D>
+__device__ __forceinline__ bool process(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t v, uint32_t src,
+                                        uint32_t &words) {
+    if (!cand_bit(P, l, v, words)) return false;
+    const uint32_t bw = P.bw[l] & ~(1u << S.cs[l][src]);
+    const uint32_t lab = P.lab[l];
+    uint32_t p = src;
+    for (int i = l - 1; i >= 0; --i) {
+        const uint32_t w = S.v[i][p];
+        if (w == v) return false;
+        if ((bw >> i) & 1u) {
+            const uint32_t row = w * P.S + lab;
+            words += 2;
+            if (!contains(P.nbr, ld_nc(P.offs + row), ld_nc(P.offs + row + 1), v, words)) return false;
+        }
+        p = S.pid[i][p];
+    }
+    return true;
+}
+
+// Walk the chain of (level, lane) and write the prefix M[0..level] into dst (by position).
+template <int D>
+__device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, uint32_t lane, uint32_t *dst) {
+    uint32_t p = lane;
+    for (int i = level; i >= 0; --i) {
+        dst[i] = S.v[i][p];
+        p = S.pid[i][p];
+    }
+}
+
+// ------------------------------------------------------------------ DFS kernel
+
+template <int D, bool ENUM>
+__global__ void __launch_bounds__(128) k_dfs(const SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    WarpStack<D> &S = reinterpret_cast<WarpStack<D> *>(smem_raw)[threadIdx.x >> 5];
+    const uint32_t lane = threadIdx.x & 31;
+    const int last = (int)P.nq - 1;
+    Ctrl *C = P.ctrl;
+    volatile Ctrl *VC = C;
+
+    unsigned long long my_count = 0, my_tasks = 0, my_rounds = 0, my_don = 0, my_words = 0;
+    uint32_t wacc = 0;
+    uint32_t tick = 0;
+    bool stop = false;
+    bool registered = false;   // this idle warp has posted a steal request
+
+    while (!stop) {
+        // ------------------------------------------------ acquire a unit of work
+        int base = 0, l = 0;
+        bool got = false;
+        uint32_t backoff = 64;
+        while (true) {
+            unsigned long long b = ~0ull, item = ~0ull;
+            int exit_now = 0;
+            if (lane == 0) {
+                if (VC->abort) {
+                    exit_now = 1;
+                } else if (VC->pool_ctr < P.pool_size) {
+                    atomicAdd(&C->work, 1);
+                    b = atomicAdd(&C->pool_ctr, (unsigned long long)P.batch);
+                    if (b >= P.pool_size) { atomicSub(&C->work, 1); b = ~0ull; }
+                }
+                if (!exit_now && b == ~0ull) {
+                    if (!P.steal) {
+                        exit_now = 1;
+                    } else {
+                        if (!registered) { atomicAdd(&C->requests, 1); registered = true; }
+                        // pop (bounded MPMC ring, per-slot sequence numbers)
+                        const unsigned long long pos = VC->q_head;
+                        const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
+                        if (seq == pos + 1 && atomicCAS(&C->q_head, pos, pos + 1) == pos) item = pos;
+                        if (item == ~0ull && VC->pool_ctr >= P.pool_size && VC->work == 0) exit_now = 1;
+                    }
+                }
+                if (b != ~0ull || item != ~0ull) registered = false;
+            }
+            b = __shfl_sync(FULL, b, 0);
+            item = __shfl_sync(FULL, item, 0);
+            exit_now = __shfl_sync(FULL, exit_now, 0);
+            if (exit_now) { stop = true; break; }
+            if (b != ~0ull) {
+                // pool batch: up to `batch` partial matches of depth d0 become the lanes of level d0-1
+                const unsigned long long k = min((unsigned long long)P.batch, P.pool_size - b);
+                const bool valid = lane < k;
+                const int d0 = (int)P.d0;
+                for (int i = 0; i < d0; ++i) {
+                    S.v[i][lane] = valid ? P.pool[(unsigned long long)i * P.pool_size + b + lane] : 0;
+                    S.pid[i][lane] = (uint8_t)lane;
+                }
+                __syncwarp();
+                generate<D>(P, S, d0, valid, lane, wacc);
+                base = d0; l = d0;
+                got = true;
+                break;
+            }
+            if (item != ~0ull) {
+                __threadfence();
+                const unsigned long long slot = item % P.q_cap;
+                const uint32_t *it = P.q_items + slot * kItemWords;
+                const uint32_t depth = __ldcg(it);     // written by another SM: read through L2
+                if (lane < depth) { S.v[lane][0] = __ldcg(it + 4 + lane); S.pid[lane][0] = 0; }
+                S.cb[depth][lane] = lane == 0 ? __ldcg(it + 1) : 0;
+                S.cl[depth][lane] = lane == 0 ? __ldcg(it + 2) : 0;
+                S.cs[depth][lane] = (uint8_t)(lane == 0 ? __ldcg(it + 3) : 0);
+                __syncwarp();
+                if (lane == 0) {   // release the slot for the next lap of the ring
+                    __threadfence();
+                    ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
+                }
+                base = (int)depth; l = (int)depth;
+                got = true;
+                break;
+            }
+            __nanosleep(backoff);
+            backoff = min(backoff * 2, 8192u);
+        }
+        if (!got) break;
+        if (lane == 0) { S.ci[l] = 0; S.cj[l] = 0; }
+        __syncwarp();
+
+        // ------------------------------------------------ depth-first batch exploration
+        while (l >= base) {
+            if (((++tick) & 31u) == 0) {
+                int ab = 0, claim = 0;
+                if (lane == 0) {
+                    if (P.deadline_ns && globaltimer() > P.deadline_ns) atomicExch(&C->abort, 1);
+                    ab = VC->abort;
+                    // work stealing (§4.3): serve one posted request by splitting our stack
+                    if (P.steal && VC->requests > 0) {
+                        if (atomicSub(&C->requests, 1) > 0) claim = 1;
+                        else atomicAdd(&C->requests, 1);
+                    }
+                }
+                if (__shfl_sync(FULL, ab, 0)) { stop = true; break; }
+                if (__shfl_sync(FULL, claim, 0)) {
+                    // shallowest level with splittable untouched work (the last level's tasks
+                    // are single checks: never worth a hand-off)
+                    int served = 0;
+                    const int top = min(l, last - 1);
+                    for (int s = base; s <= top && !served; ++s) {
+                        const uint32_t ci = S.ci[s], cj = S.cj[s];
+                        if (ci >= 32) continue;
+                        const uint32_t cl = S.cl[s][lane];
+                        // worth a hand-off: >= 2 levels left below s, or >= 256 untouched tasks
+                        const uint32_t myrem = lane > ci ? cl : (lane == ci ? cl - cj : 0u);
+                        const uint32_t remtot = __reduce_add_sync(FULL, min(myrem, 1u << 20));
+                        if (last - s < 2 && remtot < 256) continue;
+                        const uint32_t mask = __ballot_sync(FULL, lane > ci && cl > 0);
+                        uint32_t giver = 32, keep = 0, give = 0, gb = 0;
+                        if (mask) {                       // hand off the last untouched parent lane
+                            giver = 31 - __clz(mask);
+                            give = __shfl_sync(FULL, cl, giver);
+                        } else {
+                            const uint32_t rem = S.cl[s][ci] - cj;
+                            if (rem >= 2) { giver = ci; keep = rem / 2; give = rem - keep; gb = cj + keep; }
+                        }
+                        if (giver == 32) continue;
+                        // reserve a ring slot
+                        unsigned long long pos = ~0ull;
+                        if (lane == 0) {
+                            atomicAdd(&C->work, 1);
+                            pos = VC->q_tail;
+                            while (true) {
+                                const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
+                                if (seq == pos) {
+                                    const unsigned long long prev = atomicCAS(&C->q_tail, pos, pos + 1);
+                                    if (prev == pos) break;
+                                    pos = prev;
+                                } else if (seq < pos) {       // full
+                                    pos = ~0ull;
+                                    break;
+                                } else {
+                                    pos = VC->q_tail;
+                                }
+                            }
+                            if (pos == ~0ull) atomicSub(&C->work, 1);
+                        }
+                        pos = __shfl_sync(FULL, pos, 0);
+                        if (pos == ~0ull) break;          // ring full: keep the work
+                        if (lane == giver) {
+                            uint32_t *it = P.q_items + (pos % P.q_cap) * kItemWords;
+                            it[0] = (uint32_t)s; it[1] = S.cb[s][giver] + gb; it[2] = give; it[3] = S.cs[s][giver];
+                            read_prefix<D>(S, s - 1, giver, it + 4);
+                            S.cl[s][giver] = mask ? 0u : gb;
+                            __threadfence();
+                            ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap] = pos + 1;
+                        }
+                        served = 1;
+                        my_don += (lane == 0);
+                    }
+                    if (!served && lane == 0) atomicAdd(&C->requests, 1);   // give the request back
+                    __syncwarp();
+                }
+            }
+
+            // ---- ScatterTask, warp-parallel: next 32 tasks of the virtual task pool at level l
+            const uint32_t ci = S.ci[l], cj = S.cj[l];
+            uint32_t rem = 0;
+            if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
+            const uint32_t r32 = min(rem, 32u);
+            uint32_t incl = r32;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(FULL, incl, o);
+                if (lane >= (uint32_t)o) incl += x;
+            }
+            const uint32_t total = __shfl_sync(FULL, incl, 31);
+            if (total == 0) { --l; continue; }       // level exhausted: backtrack
+            const uint32_t k = min(total, 32u);
+            // source lane of task `lane` = number of lanes whose inclusive count is <= lane
+            uint32_t src = 0;
+#pragma unroll
+            for (uint32_t b = 16; b >= 1; b >>= 1) {
+                const uint32_t x = __shfl_sync(FULL, incl, src + b - 1);
+                if (x <= lane) src += b;
+            }
+            src = min(src, 31u);
+            const uint32_t src_excl = __shfl_sync(FULL, incl - r32, src);
+            const bool has = lane < k;
+            const uint32_t off = has ? lane - src_excl + (src == ci ? cj : 0) : 0;
+            const uint32_t v = has ? ld_nc(P.nbr + S.cb[l][src] + off) : 0;
+            const uint32_t lsrc = __shfl_sync(FULL, src, k - 1);
+            const uint32_t loff = __shfl_sync(FULL, off, k - 1);
+            if (lane == 0) {
+                if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
+                else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
+            }
+            my_rounds += (lane == 0);
+            my_tasks += has;
+
+            // ---- Process
+            const bool F = has && process<D>(P, S, l, v, src, wacc);
+            my_words += wacc + (has ? 1u : 0u);
+            wacc = 0;
+            if (l == last) {
+                if (ENUM) {
+                    const uint32_t fm = __ballot_sync(FULL, F);
+                    unsigned long long basepos = 0;
+                    if (lane == 0 && fm) basepos = atomicAdd(&C->out_ctr, (unsigned long long)__popc(fm));
+                    basepos = __shfl_sync(FULL, basepos, 0);
+                    if (F) {
+                        const unsigned long long idx = basepos + __popc(fm & ((1u << lane) - 1));
+                        if (idx < P.out_cap) {
+                            uint32_t *row = P.out + idx * P.nq;
+                            row[P.col[l]] = v;
+                            uint32_t p = src;
+                            for (int i = l - 1; i >= 0; --i) { row[P.col[i]] = S.v[i][p]; p = S.pid[i][p]; }
+                        }
+                    }
+                }
+                my_count += F;
+                __syncwarp();
+                continue;
+            }
+            if (has) { S.v[l][lane] = v; S.pid[l][lane] = (uint8_t)src; }
+            const uint32_t fm = __ballot_sync(FULL, F);
+            __syncwarp();
+            if (!fm) continue;
+            // ---- descend: GenerateTask for level l+1 on the lanes that extended
+            generate<D>(P, S, l + 1, F, lane, wacc);
+            if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
+            __syncwarp();
+            ++l;
+        }
+        if (lane == 0) atomicSub(&C->work, 1);
+    }
+    // flush counters
+    my_words += wacc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        my_count += __shfl_xor_sync(FULL, my_count, o);
+        my_tasks += __shfl_xor_sync(FULL, my_tasks, o);
+        my_words += __shfl_xor_sync(FULL, my_words, o);
+    }
+    if (lane == 0) {
+        if (my_count) atomicAdd(&C->count, my_count);
+        atomicAdd(&C->tasks, my_tasks);
+        atomicAdd(&C->words, my_words);
+        atomicAdd(&C->rounds, my_rounds);
+        if (my_don) atomicAdd(&C->donations, my_don);
+    }
+}
+
+// ------------------------------------------------------------------ BFS expansion
+
+// One warp per partial match of depth d (level-major input).  MODE 0: count children
+// into ctrl->count.  MODE 1: write children (depth d+1, level-major, stride out_stride).
+// MODE 2: write children as final enumerate rows (by query-vertex column).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint32_t *__restrict__ in,
+                                                unsigned long long nin, uint32_t d, uint32_t *__restrict__ outp,
+                                                unsigned long long out_stride, unsigned long long out_cap,
+                                                unsigned long long *__restrict__ ctr) {
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const uint32_t bw = P.bw[d], lab = P.lab[d];
+    unsigned long long local = 0;
+    uint32_t scratch = 0;   // word counter (unused: the BFS phase is not part of the DFS roofline)
+    for (unsigned long long it = warp; it < nin; it += nwarps) {
+        const uint32_t m = lane < d ? in[(unsigned long long)lane * nin + it] : 0;
+        uint32_t lo = 0, hi = 0, len = 0xffffffffu;
+        if (lane < d && ((bw >> lane) & 1u)) {
+            const uint32_t row = m * P.S + lab;
+            lo = ld_nc(P.offs + row); hi = ld_nc(P.offs + row + 1); len = hi - lo;
+        }
+        // source = backward neighbour with the shortest slice (ties: deepest level)
+        uint32_t best = len, bl = lane;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint32_t ob = __shfl_xor_sync(FULL, best, o), oll = __shfl_xor_sync(FULL, bl, o);
+            if (ob < best || (ob == best && oll > bl)) { best = ob; bl = oll; }
+        }
+        const uint32_t cb = __shfl_sync(FULL, lo, bl);
+        const uint32_t checks = bw & ~(1u << bl);
+        for (uint32_t j0 = 0; j0 < best; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            bool F = j < best;
+            const uint32_t v = F ? ld_nc(P.nbr + cb + j) : 0;
+            if (F) F = cand_bit(P, d, v, scratch);
+            for (uint32_t i = 0; i < d; ++i) {
+                const uint32_t mi = __shfl_sync(FULL, m, i);
+                const uint32_t loi = __shfl_sync(FULL, lo, i), hii = __shfl_sync(FULL, hi, i);
+                if (F && v == mi) F = false;
+                if (F && ((checks >> i) & 1u)) F = contains(P.nbr, loi, hii, v, scratch);
+            }
+            const uint32_t fm = __ballot_sync(FULL, F);
+            if (MODE == 0) {
+                local += __popc(fm);
+            } else if (fm) {
+                unsigned long long basepos = 0;
+                if (lane == 0) basepos = atomicAdd(ctr, (unsigned long long)__popc(fm));
+                basepos = __shfl_sync(FULL, basepos, 0);
+                const unsigned long long pos = basepos + __popc(fm & ((1u << lane) - 1));
+                const bool wr = F && pos < out_cap;
+                for (uint32_t i = 0; i < d; ++i) {
+                    const uint32_t mi = __shfl_sync(FULL, m, i);
+                    if (wr) {
+                        if (MODE == 1) outp[i * out_stride + pos] = mi;
+                        else outp[pos * P.nq + P.col[i]] = mi;
+                    }
+                }
+                if (wr) {
+                    if (MODE == 1) outp[d * out_stride + pos] = v;
+                    else outp[pos * P.nq + P.col[d]] = v;
+                }
+            }
+        }
+    }
+    if (MODE == 0 && lane == 0 && local) atomicAdd(ctr, local);
+}
+
+// Root candidates owned by this rank: cand bit of phi[0] set and (v / chunk) % world == rank.
+__global__ void k_roots(const SearchParams P, unsigned long long n, const uint32_t *__restrict__ user,
+                        unsigned long long nuser, uint32_t rank, uint32_t world, uint32_t chunk,
+                        uint32_t *__restrict__ out, unsigned long long *__restrict__ ctr,
+                        const uint32_t *__restrict__ vlab) {
+    const unsigned long long total = user ? nuser : n;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long v = user ? user[i] : i;
+        bool ok = v < n && (v / chunk) % world == rank;
+        uint32_t scratch = 0;
+        if (ok) ok = vlab[v] == P.lab[0] && cand_bit(P, 0, (uint32_t)v, scratch);
+        if (ok) out[atomicAdd(ctr, 1ull)] = (uint32_t)v;
+    }
+}
+
+__global__ void k_write_single(const uint32_t *__restrict__ roots, unsigned long long n, uint32_t *__restrict__ out,
+                               unsigned long long cap) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n && i < cap;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        out[i] = roots[i];
+}
+
+__global__ void k_read_timer(unsigned long long *t) { *t = globaltimer(); }
+
+__global__ void k_init_ring(unsigned long long *seq, unsigned long long cap) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < cap;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        seq[i] = i;
+}
+
+// ------------------------------------------------------------------ host orchestration
+
+struct Workspace {
+    Ctrl *ctrl = nullptr;
+    uint32_t *q_items = nullptr;
+    unsigned long long *q_seq = nullptr;
+    unsigned long long q_cap = 0;
+    uint32_t *buf[2] = {nullptr, nullptr};
+    size_t buf_bytes[2] = {0, 0};
+    int sms = 148;
+    ~Workspace() {
+        cudaFree(ctrl); cudaFree(q_items); cudaFree(q_seq); cudaFree(buf[0]); cudaFree(buf[1]);
+    }
+};
+
+static int ensure(uint32_t *&p, size_t &have, size_t need) {
+    if (have >= need) return GM_OK;
+    cudaFree(p);
+    p = nullptr;
+    have = 0;
+    size_t want = need + need / 4;
+    GM_CK(cudaMalloc(&p, want));
+    have = want;
+    return GM_OK;
+}
+
+template <int D>
+static size_t stack_bytes() { return sizeof(WarpStack<D>); }
+
+template <int D, bool ENUM>
+static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, cudaStream_t st,
+                      uint32_t *grid_out, uint32_t *block_out) {
+    const size_t smem = stack_bytes<D>() * wpb;
+    auto kern = k_dfs<D, ENUM>;
+    GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int fit = 0;
+    GM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, (int)(wpb * 32), smem));
+    GM_REQ(fit > 0, GM_ERR_LIMIT, "k_dfs: no block fits (smem %zu)", smem);
+    const int per = bps ? std::min<int>((int)bps, fit) : fit;
+    const uint32_t grid = (uint32_t)(sms * per);
+    // pool items per fetch: 32 (a full warp of parent lanes) when the pool is large; fewer
+    // when it is small, so that every warp gets some initial work (§4.3).
+    const unsigned long long nwarps = (unsigned long long)grid * wpb;
+    const unsigned long long per_warp = P.pool_size / (4 * nwarps);
+    P.batch = (uint32_t)std::max<unsigned long long>(1, std::min<unsigned long long>(32, per_warp));
+    kern<<<grid, wpb * 32, smem, st>>>(P);
+    GM_CK(cudaGetLastError());
+    *grid_out = grid;
+    *block_out = wpb * 32;
+    return GM_OK;
+}
+
+static int grid_for(unsigned long long work_items, int per_block, int sms) {
+    unsigned long long g = (work_items + per_block - 1) / per_block;
+    unsigned long long cap = (unsigned long long)sms * 16;
+    if (g > cap) g = cap;
+    return (int)(g ? g : 1);
+}
+
+}  // namespace gm
+
+using namespace gm;
+
+// Per-device search workspace (control block, steal ring, BFS pool buffers), created on
+// first use and reused by every later search on that device, so that steady-state
+// queries allocate nothing.  Searches on one device are serialised by its mutex.
+struct DeviceWorkspace {
+    std::mutex mu;
+    Workspace *ws = nullptr;
+};
+static DeviceWorkspace g_ws[64];
+
+static Workspace *device_workspace(int dev) {
+    DeviceWorkspace &d = g_ws[dev & 63];
+    if (!d.ws) {
+        d.ws = new Workspace();
+        cudaDeviceGetAttribute(&d.ws->sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return d.ws;
+}
+
+extern "C" void gm_default_opts(gm_run_opts *o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->tau = 1000000;
+    o->world = 1;
+    o->root_chunk = 64;
+    o->steal = 1;
+    o->warps_per_block = 4;
+    o->pool_bytes_max = 1ull << 30;
+}
+
+static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumerate, uint32_t *out, uint64_t cap,
+                      int mem, uint64_t *count_out, int count_mem, gm_run_stats *stats, cudaStream_t st) {
+    set_error("");
+    GM_REQ(p && p->g, GM_ERR_ARG, "gm_count: NULL plan");
+    GM_REQ(count_out, GM_ERR_ARG, "gm_count: NULL count_out");
+    GM_REQ(mem == GM_MEM_HOST || mem == GM_MEM_DEVICE, GM_ERR_ARG, "bad mem");
+    GM_REQ(count_mem == GM_MEM_HOST || count_mem == GM_MEM_DEVICE, GM_ERR_ARG, "bad mem");
+    gm_run_opts o;
+    gm_default_opts(&o);
+    if (opts_in) {
+        o = *opts_in;
+        if (!o.tau) o.tau = 1000000;
+        if (!o.world) o.world = 1;
+        if (!o.root_chunk) o.root_chunk = 64;
+        if (!o.warps_per_block) o.warps_per_block = 4;
+        if (!o.pool_bytes_max) o.pool_bytes_max = 1ull << 30;
+    }
+    GM_REQ(o.rank < o.world, GM_ERR_ARG, "rank %u >= world %u", o.rank, o.world);
+    GM_REQ(o.warps_per_block <= 32, GM_ERR_ARG, "warps_per_block > 32");
+    GM_REQ(o.num_roots == 0 || o.roots, GM_ERR_ARG, "num_roots > 0 but roots NULL");
+    const gm_graph *g = p->g;
+    int dev = 0;
+    GM_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_ws[dev & 63].mu);
+    Workspace &W = *device_workspace(dev);
+    gm_run_stats rs;
+    memset(&rs, 0, sizeof(rs));
+    uint32_t launches = 0;
+
+    cudaEvent_t e0, e1, d0e, d1e;
+    GM_CK(cudaEventCreate(&e0)); GM_CK(cudaEventCreate(&e1));
+    GM_CK(cudaEventCreate(&d0e)); GM_CK(cudaEventCreate(&d1e));
+    GM_CK(cudaEventRecord(e0, st));
+
+    SearchParams P;
+    memset(&P, 0, sizeof(P));
+    P.offs = g->offs; P.nbr = g->nbr; P.cand = p->cand;
+    P.S = g->S; P.nq = p->nq; P.words = p->words; P.use_cand = 1;
+    for (uint32_t l = 0; l < p->nq; ++l) {
+        P.lab[l] = p->qlab[p->order[l]] < g->S ? p->qlab[p->order[l]] : 0xfffffffeu;
+        P.bw[l] = p->bw[l];
+        P.candoff[l] = p->order[l] * p->words;
+        P.col[l] = p->order[l];
+    }
+    if (!W.ctrl) GM_CK(cudaMalloc(&W.ctrl, sizeof(Ctrl)));
+    GM_CK(cudaMemsetAsync(W.ctrl, 0, sizeof(Ctrl), st));
+    P.ctrl = W.ctrl;
+    unsigned long long *ctr_count = &W.ctrl->count;
+    unsigned long long *ctr_aux = &W.ctrl->out_ctr;
+
+    // ---- root candidates (rank share)
+    uint32_t *d_user = nullptr;
+    const unsigned long long nroot_cap = o.num_roots ? o.num_roots : g->n;
+    int rc = ensure(W.buf[0], W.buf_bytes[0], sizeof(uint32_t) * (nroot_cap ? nroot_cap : 1));
+    if (rc) return rc;
+    if (o.num_roots) {
+        GM_CK(cudaMalloc(&d_user, sizeof(uint32_t) * o.num_roots));
+        GM_CK(cudaMemcpyAsync(d_user, o.roots, sizeof(uint32_t) * o.num_roots, cudaMemcpyHostToDevice, st));
+    }
+    if (nroot_cap) {
+        k_roots<<<grid_for(nroot_cap, 256, W.sms), 256, 0, st>>>(P, g->n, d_user, o.num_roots, o.rank, o.world,
+                                                                  o.root_chunk, W.buf[0], ctr_aux, g->lab);
+        GM_CK(cudaGetLastError());
+        ++launches;
+    }
+    unsigned long long nroots = 0;
+    GM_CK(cudaMemcpyAsync(&nroots, ctr_aux, sizeof(nroots), cudaMemcpyDeviceToHost, st));
+    GM_CK(cudaStreamSynchronize(st));
+    if (d_user) cudaFree(d_user);
+    rs.roots = nroots;
+
+    uint32_t *frontier = W.buf[0];
+    int cur = 0;
+    unsigned long long P_n = nroots;
+    uint32_t d = 1;
+    unsigned long long total = 0;
+    bool done = false;
+    unsigned long long zero = 0;
+
+    if (p->nq == 1) {
+        total = nroots;
+        if (enumerate && nroots) {
+            uint32_t *dst = out;
+            uint32_t *tmp = nullptr;
+            if (mem == GM_MEM_HOST) { GM_CK(cudaMalloc(&tmp, sizeof(uint32_t) * std::max<uint64_t>(1, std::min<uint64_t>(cap, nroots)))); dst = tmp; }
+            k_write_single<<<grid_for(nroots, 256, W.sms), 256, 0, st>>>(frontier, nroots, dst, cap);
+            ++launches;
+            if (tmp) {
+                GM_CK(cudaMemcpyAsync(out, tmp, sizeof(uint32_t) * std::min<uint64_t>(cap, nroots), cudaMemcpyDeviceToHost, st));
+                GM_CK(cudaStreamSynchronize(st));
+                cudaFree(tmp);
+            }
+        }
+        done = true;
+    }
+    uint32_t *enum_dev = nullptr;   // device staging for host-side enumerate output
+    auto out_dev = [&]() -> uint32_t * {
+        if (mem == GM_MEM_DEVICE) return out;
+        if (!enum_dev && cap) cudaMalloc(&enum_dev, sizeof(uint32_t) * cap * p->nq);
+        return enum_dev;
+    };
+
+    // ---- initialization phase: BFS to tau partial matches (§4.3)
+    while (!done) {
+        if (P_n == 0) { total = 0; done = true; break; }
+        if (P_n >= o.tau) break;
+        GM_CK(cudaMemcpyAsync(ctr_count, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+        const int gb = grid_for(P_n * 32, 256, W.sms);
+        k_expand<0><<<gb, 256, 0, st>>>(P, frontier, P_n, d, nullptr, 0, 0, ctr_count);
+        GM_CK(cudaGetLastError());
+        ++launches;
+        unsigned long long c = 0;
+        GM_CK(cudaMemcpyAsync(&c, ctr_count, sizeof(c), cudaMemcpyDeviceToHost, st));
+        GM_CK(cudaStreamSynchronize(st));
+        if (d + 1 == p->nq) {
+            total = c;
+            if (enumerate && c && cap) {
+                GM_CK(cudaMemcpyAsync(ctr_aux, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+                k_expand<2><<<gb, 256, 0, st>>>(P, frontier, P_n, d, out_dev(), 0, cap, ctr_aux);
+                GM_CK(cudaGetLastError());
+                ++launches;
+            }
+            done = true;
+            break;
+        }
+        const size_t need = sizeof(uint32_t) * (size_t)c * (d + 1);
+        if (c == 0) { total = 0; done = true; break; }
+        if (need > o.pool_bytes_max) break;
+        rc = ensure(W.buf[cur ^ 1], W.buf_bytes[cur ^ 1], need);
+        if (rc) return rc;
+        GM_CK(cudaMemcpyAsync(ctr_aux, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+        k_expand<1><<<gb, 256, 0, st>>>(P, frontier, P_n, d, W.buf[cur ^ 1], c, c, ctr_aux);
+        GM_CK(cudaGetLastError());
+        ++launches;
+        cur ^= 1;
+        frontier = W.buf[cur];
+        P_n = c;
+        ++d;
+    }
+    rs.pool_size = P_n;
+    rs.pool_depth = d;
+
+    // ---- DFS (fine-grained, batch exploration, stealing)
+    if (!done) {
+        if (o.steal && !W.q_items) {
+            W.q_cap = 1u << 18;
+            GM_CK(cudaMalloc(&W.q_items, sizeof(uint32_t) * (size_t)W.q_cap * kItemWords));
+            GM_CK(cudaMalloc(&W.q_seq, sizeof(unsigned long long) * (size_t)W.q_cap));
+        }
+        if (o.steal) {
+            k_init_ring<<<grid_for(W.q_cap, 256, W.sms), 256, 0, st>>>(W.q_seq, W.q_cap);
+            GM_CK(cudaGetLastError());
+            ++launches;
+        }
+        GM_CK(cudaMemsetAsync(W.ctrl, 0, sizeof(Ctrl), st));
+        P.pool = frontier;
+        P.pool_size = P_n;
+        P.d0 = d;
+        P.steal = o.steal ? 1 : 0;
+        P.q_items = W.q_items; P.q_seq = W.q_seq; P.q_cap = o.steal ? W.q_cap : 1;
+        if (enumerate) { P.out = out_dev(); P.out_cap = cap; }
+        unsigned long long deadline = 0;
+        if (o.time_limit_ms > 0) {
+            // deadline on the device's %globaltimer clock (ns), read by a 1-thread kernel
+            unsigned long long *d_t = &W.ctrl->tasks;   // scratch (zeroed below)
+            k_read_timer<<<1, 1, 0, st>>>(d_t);
+            GM_CK(cudaMemcpyAsync(&deadline, d_t, sizeof(deadline), cudaMemcpyDeviceToHost, st));
+            GM_CK(cudaStreamSynchronize(st));
+            deadline += (unsigned long long)(o.time_limit_ms * 1e6);
+            GM_CK(cudaMemsetAsync(d_t, 0, sizeof(unsigned long long), st));
+            ++launches;
+        }
+        P.deadline_ns = deadline;
+        GM_CK(cudaEventRecord(d0e, st));
+        const uint32_t nq = p->nq;
+        if (nq <= 8)
+            rc = enumerate ? launch_dfs<8, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block)
+                           : launch_dfs<8, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block);
+        else if (nq <= 16)
+            rc = enumerate ? launch_dfs<16, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block)
+                           : launch_dfs<16, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block);
+        else
+            rc = enumerate ? launch_dfs<32, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block)
+                           : launch_dfs<32, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block);
+        if (rc) return rc;
+        ++launches;
+        rs.dfs_launches = 1;
+        GM_CK(cudaEventRecord(d1e, st));
+        Ctrl h;
+        GM_CK(cudaMemcpyAsync(&h, W.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
+        GM_CK(cudaStreamSynchronize(st));
+        total = h.count;
+        rs.tasks = h.tasks;
+        rs.words = h.words;
+        rs.rounds = h.rounds;
+        rs.donations = h.donations;
+        rs.timed_out = h.abort ? 1 : 0;
+        GM_CK(cudaEventElapsedTime(&rs.dfs_ms, d0e, d1e));
+    }
+    // ---- outputs
+    if (enumerate && mem == GM_MEM_HOST && enum_dev && cap) {
+        const uint64_t rows = std::min<uint64_t>(cap, total);
+        GM_CK(cudaMemcpyAsync(out, enum_dev, sizeof(uint32_t) * rows * p->nq, cudaMemcpyDeviceToHost, st));
+    }
+    if (count_mem == GM_MEM_DEVICE) {
+        GM_CK(cudaMemcpyAsync(ctr_count, &total, sizeof(total), cudaMemcpyHostToDevice, st));
+        GM_CK(cudaMemcpyAsync(count_out, ctr_count, sizeof(total), cudaMemcpyDeviceToDevice, st));
+    } else {
+        *count_out = total;
+    }
+    GM_CK(cudaEventRecord(e1, st));
+    GM_CK(cudaStreamSynchronize(st));
+    if (enum_dev) cudaFree(enum_dev);
+    GM_CK(cudaEventElapsedTime(&rs.total_ms, e0, e1));
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(d0e); cudaEventDestroy(d1e);
+    rs.count = total;
+    rs.kernel_launches = launches;
+    if (stats) *stats = rs;
+    return rs.timed_out ? GM_TIMEOUT : GM_OK;
+}
+
+extern "C" int gm_count(const gm_plan *p, const gm_run_opts *opts, uint64_t *count_out, int mem,
+                        gm_run_stats *stats, void *stream) {
+    return run_search(p, opts, false, nullptr, 0, GM_MEM_DEVICE, count_out, mem, stats, (cudaStream_t)stream);
+}
+
+extern "C" int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t *out, uint64_t capacity, int mem,
+                            uint64_t *count_host, gm_run_stats *stats, void *stream) {
+    GM_REQ(capacity == 0 || out, GM_ERR_ARG, "gm_enumerate: out NULL with capacity > 0");
+    return run_search(p, opts, true, out, capacity, mem, count_host, GM_MEM_HOST, stats, (cudaStream_t)stream);
+}

@@ -1,0 +1,338 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Counts must be bit-exact; enumerations must equal the oracle's sorted embedding set;
+CSR and candidate bitmaps must be bit-exact against definitions computed by the oracle.
+Inputs are the seeded generators of gminputs (shared by both sides).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gminputs as gi
+from conftest import load_fig1
+from oracle import OracleGraph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2604_10601_b200 as gm
+    return gm
+
+
+def sorted_rows(a):
+    a = np.asarray(a, dtype=np.uint32)
+    if len(a) == 0:
+        return a.reshape(0, a.shape[1] if a.ndim == 2 else 0)
+    return a[np.lexsort(a.T[::-1])]
+
+
+def small_random_query(seed, k, nl):
+    rs = np.random.default_rng(seed + 991)
+    edges = {(int(rs.integers(0, v)), v) for v in range(1, k)}
+    for a in range(k):
+        for b in range(a + 1, k):
+            if rs.random() < 0.3:
+                edges.add((a, b))
+    return gi.Query(k, sorted(edges), rs.integers(0, nl, k).tolist())
+
+
+# ------------------------------------------------------------------ graph build
+
+@pytest.mark.parametrize("seed,nl", [(0, 1), (1, 3), (2, 8)])
+def test_csr_matches_oracle(gm, seed, nl):
+    n, s, d = gi.rmat_edges(10, 8, seed)
+    lab = gi.uniform_labels(n, nl, seed)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    offs, nbr, glab = g.export()
+    off_o, adj_o = OracleGraph(n, s, d, lab).csr()
+    assert np.array_equal(glab, lab)
+    assert g.info()["num_adj"] == len(adj_o)
+    assert g.info()["d_max"] == int(np.diff(off_o).max())
+    for v in range(n):
+        row = adj_o[off_o[v]:off_o[v + 1]]
+        # label-partitioned: rows v*nl + l are the label-l neighbours of v, ascending
+        for l in range(nl):
+            mine = nbr[offs[v * nl + l]:offs[v * nl + l + 1]]
+            assert np.array_equal(mine, row[lab[row] == l])
+
+
+def test_csr_edge_cases(gm):
+    # self loops, duplicates, isolated vertices, empty graph
+    g = gm.gm_load_graph(5, np.array([0, 0, 1, 3, 1], np.uint32), np.array([0, 1, 0, 3, 2], np.uint32))
+    offs, nbr, _ = g.export()
+    assert offs.tolist() == [0, 1, 3, 4, 4, 4] and nbr.tolist() == [1, 0, 2, 1]
+    g0 = gm.gm_load_graph(4, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+    assert g0.info()["num_adj"] == 0
+    with pytest.raises(gm.GMError):
+        gm.gm_load_graph(3, np.array([0], np.uint32), np.array([5], np.uint32))
+    with pytest.raises(gm.GMError):
+        gm.gm_load_graph(3, np.array([0], np.uint32), np.array([1], np.uint32), np.array([0, 1, 7], np.uint32), 2)
+
+
+def test_gpu_generator_matches_numpy(gm):
+    import gminputs.gpu as gg
+    n, s, d = gi.rmat_edges(12, 4, seed=9)
+    n2, s2, d2 = gg.rmat_edges(12, 4, seed=9)
+    assert n == n2
+    assert np.array_equal(s, s2.cpu().numpy().view(np.uint32)) and np.array_equal(d, d2.cpu().numpy().view(np.uint32))
+    n, s, d = gi.er_edges(3000, 6, seed=4)
+    _, s2, d2 = gg.er_edges(3000, 6, seed=4)
+    assert np.array_equal(s, s2.cpu().numpy().view(np.uint32)) and np.array_equal(d, d2.cpu().numpy().view(np.uint32))
+    assert np.array_equal(gi.uniform_labels(5000, 7, 3), gg.uniform_labels(5000, 7, 3).cpu().numpy().view(np.uint32))
+
+
+def test_device_resident_load_equals_host_load(gm):
+    import gminputs.gpu as gg
+    n, s, d = gg.rmat_edges(11, 8, seed=3)
+    lab = gg.uniform_labels(n, 4, 3)
+    g1 = gm.gm_load_graph(n, s, d, lab, 4)
+    g2 = gm.gm_load_graph(n, s.cpu().numpy().view(np.uint32), d.cpu().numpy().view(np.uint32),
+                          lab.cpu().numpy().view(np.uint32), 4)
+    for a, b in zip(g1.export(), g2.export()):
+        assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ filter
+
+@pytest.mark.parametrize("seed", range(4))
+def test_filter_bitmaps_match_oracle(gm, seed):
+    n, s, d = gi.er_edges(700, 7, seed)
+    nl = 3
+    lab = gi.uniform_labels(n, nl, seed)
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    q = small_random_query(seed, 6, nl)
+    for kind in ("ldf", "nlf"):
+        ref = og.filter(q, kind, nl)
+        p = gm.gm_plan_query(g, q, filter=kind)
+        for u in range(q.n):
+            assert np.array_equal(p.candidates(u), ref[u].astype(bool)), (kind, u)
+        assert p.info()["cand_count"] == [int(x) for x in ref.sum(1)]
+    p = gm.gm_plan_query(g, q, filter="none")
+    for u in range(q.n):
+        assert np.array_equal(p.candidates(u), lab == q.labels[u])
+
+
+def test_plan_order_is_connected_and_user_order_validated(gm):
+    n, s, d = gi.er_edges(200, 6, 1)
+    g = gm.gm_load_graph(n, s, d)
+    q = gi.Query(4, [(0, 1), (1, 2), (2, 3)], [0, 0, 0, 0])
+    info = gm.gm_plan_query(g, q).info()
+    order = info["order"]
+    assert sorted(order) == [0, 1, 2, 3]
+    for i in range(1, 4):
+        assert info["backward"][i] != 0
+    with pytest.raises(gm.GMError):
+        gm.gm_plan_query(g, q, order=[0, 2, 1, 3])      # 2 has no earlier neighbour
+    with pytest.raises(gm.GMError):
+        gm.gm_plan_query(g, gi.Query(4, [(0, 1), (2, 3)], [0] * 4))   # disconnected query
+
+
+# ------------------------------------------------------------------ counts and enumeration
+
+def run_both(gm, n, s, d, lab, nl, q, **kw):
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    p = gm.gm_plan_query(g, q, filter=kw.pop("filter", "nlf"), order=kw.pop("order", None))
+    c, st = gm.gm_count(p, **kw)
+    return og.count(q), c, st, og, g, p
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_count_random_small(gm, seed):
+    nl = [1, 2, 4][seed % 3]
+    if seed % 2:
+        n, s, d = gi.er_edges(300 + 20 * seed, 6 + seed % 5, seed)
+    else:
+        n, s, d = gi.rmat_edges(9, 6, seed)
+    lab = gi.uniform_labels(n, nl, seed)
+    k = 3 + seed % 4
+    q = small_random_query(seed, k, nl)
+    tau = [1, 64, 1000000][seed % 3]
+    ref, c, st, *_ = run_both(gm, n, s, d, lab, nl, q, tau=tau, steal=bool(seed % 4 != 1))
+    assert c == ref, (q.edges.tolist(), q.labels.tolist(), st)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_enumerate_random_small(gm, seed):
+    nl = [1, 2, 3][seed % 3]
+    n, s, d = gi.er_edges(150, 6, seed)
+    lab = gi.uniform_labels(n, nl, seed)
+    q = small_random_query(seed, 3 + seed % 3, nl)
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    p = gm.gm_plan_query(g, q)
+    ref = og.enumerate(q)
+    rows, total, _ = gm.gm_enumerate(p, capacity=len(ref) + 5, tau=[1, 32, 10 ** 6][seed % 3])
+    assert total == len(ref)
+    assert np.array_equal(sorted_rows(rows), ref)
+
+
+def test_figure1_example(gm):
+    n, s, d, lab, q, exp = load_fig1()
+    g = gm.gm_load_graph(n, s, d, lab, 4)
+    for tau in (1, 4, 10 ** 6):
+        p = gm.gm_plan_query(g, q)
+        c, _ = gm.gm_count(p, tau=tau)
+        assert c == 112
+        rows, total, _ = gm.gm_enumerate(p, capacity=200, tau=tau)
+        assert total == 112 and tuple(exp["match"]) in {tuple(int(x) for x in r) for r in rows}
+    # the paper's order phi = (u1,u2,u3,u4) (line 197)
+    p = gm.gm_plan_query(g, q, order=[0, 1, 2, 3])
+    assert gm.gm_count(p, tau=1)[0] == 112
+
+
+@pytest.mark.parametrize("n,k", [(6, 3), (8, 4), (9, 5), (10, 6), (12, 3)])
+def test_clique_closed_form(gm, n, k):
+    nn, s, d = gi.complete_graph(n)
+    g = gm.gm_load_graph(nn, s, d)
+    for tau in (1, 10 ** 6):
+        c, _ = gm.gm_count(gm.gm_plan_query(g, gi.clique(k)), tau=tau)
+        assert c == math.factorial(n) // math.factorial(n - k)
+
+
+def test_cycle_and_path_closed_forms(gm):
+    n = 40
+    g = gm.gm_load_graph(*gi.cycle_graph(n))
+    assert gm.gm_count(gm.gm_plan_query(g, gi.cycle(n // 2)))[0] == 0
+    for k in (2, 5, 17, 32):                       # 32 = GM_MAX_QUERY
+        assert gm.gm_count(gm.gm_plan_query(g, gi.path(k)), tau=1)[0] == 2 * n
+    g = gm.gm_load_graph(*gi.cycle_graph(32))
+    assert gm.gm_count(gm.gm_plan_query(g, gi.cycle(32)), tau=1)[0] == 64
+
+
+def test_star_closed_form_with_hub(gm):
+    # star with a 5000-leaf hub: d_max >> 32, one root -> relies on batching + stealing
+    n, s, d = gi.star_graph(5000)
+    g = gm.gm_load_graph(n, s, d)
+    for steal in (True, False):
+        c, st = gm.gm_count(gm.gm_plan_query(g, gi.star(2)), tau=1, steal=steal)
+        assert c == 5000 * 4999 + 0
+    c, _ = gm.gm_count(gm.gm_plan_query(g, gi.path(3)), tau=1)
+    assert c == 5000 * 4999
+
+
+def test_edge_cases(gm):
+    n, s, d = gi.er_edges(100, 4, 2)
+    lab = gi.uniform_labels(n, 2, 2)
+    g = gm.gm_load_graph(n, s, d, lab, 2)
+    og = OracleGraph(n, s, d, lab)
+    # single-vertex query: every vertex with the label
+    q1 = gi.Query(1, [], [1])
+    assert gm.gm_count(gm.gm_plan_query(g, q1))[0] == int((lab == 1).sum())
+    rows, total, _ = gm.gm_enumerate(gm.gm_plan_query(g, q1), capacity=1000)
+    assert sorted(rows[:, 0].tolist()) == np.flatnonzero(lab == 1).tolist()
+    # label absent from G
+    q = gi.Query(3, [(0, 1), (1, 2)], [0, 5, 0])
+    assert gm.gm_count(gm.gm_plan_query(g, q))[0] == 0
+    # single edge query
+    q2 = gi.Query(2, [(0, 1)], [0, 1])
+    assert gm.gm_count(gm.gm_plan_query(g, q2))[0] == og.count(q2)
+    # query larger than any component
+    gsmall = gm.gm_load_graph(*gi.path_graph(4))
+    assert gm.gm_count(gm.gm_plan_query(gsmall, gi.path(5)))[0] == 0
+    # empty graph
+    g0 = gm.gm_load_graph(10, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+    assert gm.gm_count(gm.gm_plan_query(g0, gi.triangle()))[0] == 0
+
+
+def test_enumerate_capacity_overflow(gm):
+    g = gm.gm_load_graph(*gi.complete_graph(7))
+    p = gm.gm_plan_query(g, gi.clique(4))
+    rows, total, _ = gm.gm_enumerate(p, capacity=100, tau=1)
+    assert total == 840 and len(rows) == 100
+    rows = rows.astype(np.int64)
+    assert all(len(set(r)) == 4 for r in rows.tolist())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_partition_sums_to_total(gm, world):
+    n, s, d = gi.rmat_edges(11, 8, 5)
+    lab = gi.uniform_labels(n, 2, 5)
+    q = gi.tailed_triangle((0, 1, 0, 1))
+    g = gm.gm_load_graph(n, s, d, lab, 2)
+    p = gm.gm_plan_query(g, q)
+    total = gm.gm_count(p)[0]
+    parts = [gm.gm_count(p, rank=r, world=world, root_chunk=16, tau=128)[0] for r in range(world)]
+    assert sum(parts) == total == OracleGraph(n, s, d, lab).count(q)
+
+
+def test_user_roots_match_oracle_fixed_root(gm):
+    n, s, d = gi.rmat_edges(12, 8, 7)
+    q = gi.clique(4)
+    g = gm.gm_load_graph(n, s, d)
+    og = OracleGraph(n, s, d)
+    p = gm.gm_plan_query(g, q)
+    u0 = p.info()["order"][0]
+    rs = np.random.default_rng(0)
+    roots = rs.choice(n, 30, replace=False).astype(np.uint32)
+    c, _ = gm.gm_count(p, roots=roots, tau=1)
+    assert c == sum(og.count(q, fixed=(u0, int(v))) for v in roots)
+
+
+def test_count_to_device_tensor(gm):
+    import torch
+    g = gm.gm_load_graph(*gi.complete_graph(6))
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    gm.gm_count(gm.gm_plan_query(g, gi.clique(3)), out=out)
+    assert int(out.item()) == 120
+
+
+def test_time_limit_reports_timeout(gm):
+    n, s, d = gi.rmat_edges(14, 16, 1)
+    g = gm.gm_load_graph(n, s, d)
+    p = gm.gm_plan_query(g, gi.path(8))
+    c, st = gm.gm_count(p, time_limit_ms=5, tau=1000)
+    assert st["timed_out"] == 1
+
+
+# ------------------------------------------------------------------ BASELINE configs (sampled)
+
+def test_config1_full(gm):
+    """configs[0]: ER(1000, avg deg 8, 4 labels), tailed triangle -- full enumeration parity."""
+    n, s, d = gi.er_edges(1000, 8, 11)
+    lab = gi.uniform_labels(n, 4, 11)
+    q = gi.tailed_triangle((0, 1, 2, 3))
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, 4)
+    p = gm.gm_plan_query(g, q)
+    ref = og.enumerate(q)
+    rows, total, _ = gm.gm_enumerate(p, capacity=len(ref) + 1)
+    assert total == len(ref) and np.array_equal(sorted_rows(rows), ref)
+
+
+def test_config2_sampled_roots(gm):
+    """configs[1]: R-MAT scale 18 (16 edges/vertex), 8 labels, 8-vertex queries (§6.1 generator):
+    GPU count restricted to sampled roots == sum of the oracle's per-root counts.  Roots are
+    sampled among phi[0]'s candidates whose oracle count stays under a budget (the oracle
+    must finish); the GPU runs in the bench launch configuration (tau = 1e6, stealing on)."""
+    n, s, d = gi.rmat_edges(18, 16, 2)
+    lab = gi.uniform_labels(n, 8, 2)
+    off, nb = gi.simple_adjacency(n, s, d)
+    g = gm.gm_load_graph(n, s, d, lab, 8)
+    og = OracleGraph(n, s, d, lab)
+    rs = np.random.default_rng(1)
+    budget = 3_000_000          # oracle search-tree nodes per sampled root
+    checked = 0
+    for qs in range(4):
+        q = (gi.random_query if qs % 2 == 0 else gi.random_walk_query)(off, nb, lab, 8, seed=100 + qs)
+        p = gm.gm_plan_query(g, q)
+        u0 = p.info()["order"][0]
+        cands = np.flatnonzero(p.candidates(u0))
+        roots, ref = [], 0
+        for v in rs.permutation(cands)[:200]:
+            c = og.count(q, fixed=(u0, int(v)), max_nodes=budget)
+            if c is not None:
+                roots.append(int(v)); ref += c
+            if len(roots) == 8:
+                break
+        c, _ = gm.gm_count(p, roots=np.array(roots, np.uint32))
+        assert c == ref, (q, roots)
+        checked += len(roots)
+    assert checked >= 16

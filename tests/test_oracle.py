@@ -211,3 +211,11 @@ def test_filter_hand_example():
     assert ldf[0].tolist() == [1, 0, 1, 1, 1]
     assert nlf[0].tolist() == [1, 0, 1, 1, 0]
     assert ldf[1].tolist() == [0, 1, 0, 0, 0] == nlf[1].tolist()
+
+
+def test_node_budget_only_discards():
+    n, src, dst = gi.er_edges(60, 8.0, 1)
+    g = OracleGraph(n, src, dst)
+    full = g.count(gi.path(4))
+    assert g.count(gi.path(4), max_nodes=10 ** 9) == full
+    assert g.count(gi.path(4), max_nodes=5) is None
