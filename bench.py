@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""bench.py -- device-timed subgraph-matching throughput (embeddings/s, query ms).
+
+Workload (BASELINE.json configs[1], the single-GPU headline config): R-MAT scale 18,
+16 sampled edges/vertex (262,144 vertices, ~3.8M undirected edges), 8 uniform labels, and
+a query set of 8-vertex queries drawn with the §6.1 procedure: 4 dense (greedy-dense
+growth, average degree >= 3) + 4 sparse (random-walk trees).  A step = the whole hot path
+for every query of the set: gm_plan_query (candidate filter + order) and gm_count
+(BFS init pool + fine-grained DFS), each query under a per-query time limit (sparse
+8-vertex trees on a power-law graph have ~1e13 embeddings; the limit bounds the step).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config rmat18|er1k|rmat22]
+
+N > 1 (torchrun): root candidates are split over ranks ((v / 64) % N == rank), every
+rank holds a replica of the graph, per-query counts are summed with ONE NCCL all-reduce
+per step; time = max over ranks of the device time.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (generator, params, labels, query size, dense seeds, sparse seeds, time limit ms)
+    "rmat18": dict(kind="rmat", scale=18, ef=16, labels=8, qsize=8, dense=[1000, 1001, 1002, 1003],
+                   sparse=[2000, 2001, 2002, 2003], limit_ms=1000.0, seed=2,
+                   desc="R-MAT scale 18 (262k vertices, ~3.8M edges, 8 labels), 8-vertex dense+sparse queries"),
+    "er1k": dict(kind="er", n=1000, deg=8, labels=4, qsize=4, dense=[], sparse=[], fixed="tailed_triangle",
+                 limit_ms=0.0, seed=11, desc="Erdos-Renyi G(n=1000, avg deg 8, 4 labels), tailed triangle"),
+    "rmat22": dict(kind="rmat", scale=22, ef=16, labels=1, qsize=0, dense=[], sparse=[],
+                   fixed=["triangle", "clique4", "cycle5"], limit_ms=5000.0, seed=3,
+                   desc="R-MAT scale 22 unlabelled (4.2M vertices, ~64M edges): triangle / 4-clique / 5-cycle"),
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def build_queries(cfg, off, nb, lab):
+    import gminputs as gi
+    qs = []
+    for s in cfg.get("dense", []):
+        qs.append(gi.random_query(off, nb, lab, cfg["qsize"], seed=s, dense=True, min_avg_degree=3.0))
+    for s in cfg.get("sparse", []):
+        qs.append(gi.random_walk_query(off, nb, lab, cfg["qsize"], seed=s))
+    fx = cfg.get("fixed")
+    if fx:
+        for name in ([fx] if isinstance(fx, str) else fx):
+            if name == "tailed_triangle":
+                qs.append(gi.tailed_triangle((0, 1, 2, 3)))
+            elif name == "triangle":
+                qs.append(gi.triangle())
+            elif name.startswith("clique"):
+                qs.append(gi.clique(int(name[6:])))
+            elif name.startswith("cycle"):
+                qs.append(gi.cycle(int(name[5:])))
+    for i, q in enumerate(qs):
+        q.name = q.name or f"q{i}"
+    return qs
+
+
+def make_graph_host(cfg):
+    import gminputs as gi
+    if cfg["kind"] == "rmat":
+        n, s, d = gi.rmat_edges(cfg["scale"], cfg["ef"], cfg["seed"])
+    else:
+        n, s, d = gi.er_edges(cfg["n"], cfg["deg"], cfg["seed"])
+    lab = gi.uniform_labels(n, cfg["labels"], cfg["seed"])
+    return n, s, d, lab
+
+
+def make_graph_device(cfg):
+    import gminputs.gpu as gg
+    if cfg["kind"] == "rmat":
+        n, s, d = gg.rmat_edges(cfg["scale"], cfg["ef"], cfg["seed"])
+    else:
+        n, s, d = gg.er_edges(cfg["n"], cfg["deg"], cfg["seed"])
+    lab = gg.uniform_labels(n, cfg["labels"], cfg["seed"])
+    return n, s, d, lab
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args, cfg, world, rank):
+    """The oracle (plain C, one host core) on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import gminputs as gi
+    from oracle import OracleGraph
+    n, s, d, lab = make_graph_host(cfg)
+    off, nb = gi.simple_adjacency(n, s, d)
+    qs = build_queries(cfg, off, nb, lab)
+    og = OracleGraph(n, s, d, lab)
+    budget_s = float(os.environ.get("GM_REF_STEP_S", "4.0"))
+    rs = np.random.default_rng(0)
+    times, counts, samples = [], [], []
+    for step in range(args.warmup + args.steps):
+        c, dt, nroots = oracle_sample(og, qs, lab, rs, budget_s)
+        if step >= args.warmup:
+            times.append(dt); counts.append(c); samples.append(nroots)
+    value = sum(counts) / sum(times)
+    line = {
+        "impl": "reference", "metric": "embeddings/sec", "value": value, "unit": "embeddings/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"]},
+        "cpu_baseline": {"value": value, "unit": "embeddings/s", "cores": 1, "kind": "oracle",
+                         "sample": f"per step: oracle per-root counts (query vertex 0 pinned) for "
+                                   f"{int(np.mean(samples))} random roots across {len(qs)} queries, "
+                                   f"~{budget_s:.0f}s of one host core"},
+        "e2e": {"value": value, "unit": "embeddings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def oracle_sample(og, qs, lab, rs, budget_s, max_nodes=1_000_000):
+    """Oracle per-root counts (query vertex 0 pinned to random roots) until ~budget_s of one
+    core is spent.  Only calls that finish within the node budget are timed and counted."""
+    c, t_done, nroots = 0, 0.0, 0
+    t_start = time.perf_counter()
+    per_q = budget_s / len(qs)
+    for q in qs:
+        tq = time.perf_counter()
+        cand = np.flatnonzero(lab == q.labels[0])
+        for v in rs.permutation(cand):
+            t0 = time.perf_counter()
+            r = og.count(q, fixed=(0, int(v)), max_nodes=max_nodes)
+            dt = time.perf_counter() - t0
+            if r is not None:
+                c += r; t_done += dt; nroots += 1
+            if time.perf_counter() - tq > per_q or time.perf_counter() - t_start > 2 * budget_s:
+                break
+    return c, max(t_done, 1e-9), nroots
+
+
+def cpu_baseline(cfg, qs, n, s, d, lab, budget_s=12.0):
+    """Oracle (one host core) on a bounded sample of this workload."""
+    from oracle import OracleGraph
+    og = OracleGraph(n, s, d, lab)
+    c, dt, nroots = oracle_sample(og, qs, lab, np.random.default_rng(0), budget_s)
+    return {"value": c / dt, "unit": "embeddings/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle per-root counts (query vertex 0 pinned) for {nroots} random roots "
+                      f"across {len(qs)} queries of this workload (roots whose search exceeds 1e6 "
+                      f"tree nodes skipped), {dt:.1f}s of one host core timed"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="rmat18", choices=sorted(CONFIGS))
+    ap.add_argument("--time-limit-ms", type=float, default=None)
+    ap.add_argument("--tau", type=float, default=1e6)
+    ap.add_argument("--no-steal", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--per-query", action="store_true", help="print per-query timings to stderr")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    limit = cfg["limit_ms"] if args.time_limit_ms is None else args.time_limit_ms
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import gminputs as gi
+    import paper_2604_10601_b200 as gm
+
+    # ---- inputs: graph generated on this GPU (replica per rank); queries from host adjacency
+    n, s_dev, d_dev, lab_dev = make_graph_device(cfg)
+    s_h = s_dev.cpu().numpy().view(np.uint32)
+    d_h = d_dev.cpu().numpy().view(np.uint32)
+    lab_h = lab_dev.cpu().numpy().view(np.uint32)
+    off, nb = gi.simple_adjacency(n, s_h, d_h)
+    qs = build_queries(cfg, off, nb, lab_h)
+    g = gm.gm_load_graph(n, s_dev, d_dev, lab_dev, cfg["labels"])
+    del s_dev, d_dev
+    ginfo = g.info()
+    stream = torch.cuda.current_stream()
+    run_kw = dict(tau=int(args.tau), rank=rank, world=world, steal=not args.no_steal, time_limit_ms=limit)
+
+    counts_dev = torch.zeros(len(qs), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(record):
+        """One pass of the hot path over the query set; returns per-query (stats, plan_ms)."""
+        out = []
+        plans = []
+        for i, q in enumerate(qs):
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p = gm.gm_plan_query(g, q, filter="nlf")
+            _, st = gm.gm_count(p, out=counts_dev[i:i + 1], **run_kw)
+            e1.record(stream)
+            plans.append(p)
+            out.append((st, e0, e1))
+        if world > 1:
+            dist.all_reduce(counts_dev)          # the one collective of the step
+        return out, plans
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(False)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    step_ms, dfs_ms, dfs_launches, words, kernel_launches = [], [], 0, 0, 0
+    total_emb, q_ms, timeouts, tasks = 0, [], 0, 0
+    per_query = []
+    for k in range(args.steps):
+        flush.zero_()                                # L2 flush outside the timed region
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        res, plans = step(True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        step_ms.append(s0.elapsed_time(s1))
+        total_emb += int(counts_dev.sum().item())
+        for i, (st, e0, e1) in enumerate(res):
+            q_ms.append(e0.elapsed_time(e1))
+            dfs_ms.append(st["dfs_ms"])
+            dfs_launches += st["dfs_launches"]
+            words += st["words"]
+            tasks += st["tasks"]
+            kernel_launches += st["kernel_launches"] + 1       # + the filter kernel of the plan
+            timeouts += st["timed_out"]
+            if k == 0:
+                per_query.append({"q": qs[i].name, "m": int(len(qs[i].edges)), "ms": round(q_ms[-1], 3),
+                                  "dfs_ms": round(st["dfs_ms"], 3), "timed_out": st["timed_out"],
+                                  "pool": st["pool_size"], "depth": st["pool_depth"],
+                                  "donations": st["donations"]})
+        del plans
+    clk = clocks.stop()
+
+    # ---- max over ranks
+    t_local = torch.tensor([sum(step_ms), sum(dfs_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    T_ms, T_dfs = float(t_local[0]), float(t_local[1])
+    w_local = torch.tensor([words, tasks, kernel_launches], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(w_local)
+    words_all, tasks_all, launches_all = (float(x) for x in w_local)
+    emb_per_step = total_emb / args.steps
+    value = total_emb / (T_ms / 1e3)
+
+    # ---- end to end through the public API with host buffers (rank-local share, wall clock)
+    e2e_emb, e2e_s, h2d, d2h = 0, 0.0, 0, 0
+    for k in range(max(1, args.steps)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        local = []
+        for q in qs:
+            p = gm.gm_plan_query(g, q, filter="nlf")      # query arrays copied H2D by the library
+            c, _ = gm.gm_count(p, **run_kw)                # count read back D2H
+            local.append(c)
+            h2d += q.edges.nbytes + q.labels.nbytes
+            d2h += 8
+        if world > 1:
+            t = torch.tensor(local, dtype=torch.int64, device=dev)
+            dist.all_reduce(t)
+            local = t.cpu().tolist()
+            d2h += 8 * len(qs)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e_s += dt
+        e2e_emb += sum(local)
+    e2e = {"value": e2e_emb / e2e_s, "unit": "embeddings/s", "h2d_bytes_per_step": h2d // max(1, args.steps),
+           "d2h_bytes_per_step": d2h // max(1, args.steps)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peaks()
+    # roofline of the dominant kernel (k_dfs): algorithmic bytes = 4 * words per launch
+    dfs_launch_ms = T_dfs / max(1, dfs_launches) if dfs_launches else None
+    bytes_per_launch = 4.0 * words_all / max(1, dfs_launches * (world if world > 1 else 1)) if dfs_launches else 0
+    achieved = (4.0 * words_all / world) / (T_dfs / 1e3) / 1e9 if T_dfs > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(args.config)
+    except Exception:
+        pass
+    line = {
+        "metric": "embeddings/sec", "value": value, "unit": "embeddings/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": T_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "queries": len(qs),
+                   "query_ms_mean": statistics.mean(q_ms), "query_ms_median": statistics.median(q_ms),
+                   "per_query_time_limit_ms": limit, "timed_out_queries_per_step": timeouts / args.steps,
+                   "embeddings_per_step": emb_per_step, "tau": int(args.tau), "steal": not args.no_steal,
+                   "filter": "nlf", "graph": {k: ginfo[k] for k in ("n", "num_adj", "num_labels", "d_max")},
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"roots split over {world} GPU(s), CSR replicated, 1 NCCL all-reduce/step"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_dfs", "launch_ms_mean": dfs_launch_ms,
+                     "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_kind,
+                     "share_of_step": T_dfs / T_ms if T_ms else None},
+        "gpu_launches": int(launches_all),
+        "tasks_per_s": tasks_all / (T_ms / 1e3),
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        n_, s_, d_, l_ = n, s_h, d_h, lab_h
+        line["cpu_baseline"] = cpu_baseline(cfg, qs, n_, s_, d_, l_)
+    if args.per_query:
+        print(json.dumps(per_query), file=sys.stderr)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

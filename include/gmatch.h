@@ -88,9 +88,21 @@ typedef struct {
     uint32_t num_labels;
     uint32_t d_max;        /* maximum degree */
     uint64_t device_bytes; /* device memory held by the graph */
+    uint32_t hubs;         /* vertices with a hub adjacency bitmap (gm_graph_build_hubs) */
+    uint32_t hub_min_degree;
 } gm_graph_info_t;
 
 GM_API int gm_graph_info(const gm_graph *g, gm_graph_info_t *info);
+
+/*
+ * gm_graph_build_hubs -- (re)build the hub adjacency index: for the highest-degree
+ * vertices (degree >= min_degree, at most budget_bytes / (4*ceil(n/32)) of them) a bitmap
+ * of N(v) over all vertex ids, used by the search to test v in N(w) with one word read
+ * instead of a binary search.  gm_load_graph builds it with a
+ * 64 MiB budget and min_degree 64; budget_bytes = 0 removes it.  Results never depend on it.
+ * Synchronizes `stream`.  Do not call while a search on this graph is running.
+ */
+GM_API int gm_graph_build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, void *stream);
 
 /*
  * gm_graph_export -- copy the CSR back to host buffers (tests, debugging).
@@ -144,6 +156,11 @@ GM_API void gm_free_plan(gm_plan *p);
 
 /* ------------------------------------------------------------------ search */
 
+/* gm_run_opts.flags */
+#define GM_FLAG_NO_SET_COUNT 1u  /* gm_count: validate every last-level candidate as its own task
+                                    (Alg. 2 as written) instead of set-counting the last level
+                                    when phi[last] has a single backward neighbour */
+
 typedef struct {
     uint64_t tau;            /* initial task-pool threshold (§4.3); 0 = 1e6 */
     uint32_t rank, world;    /* this rank's share of the root candidates: vertex v is
@@ -157,6 +174,7 @@ typedef struct {
                                 these vertices (still filtered and rank-partitioned) */
     uint64_t num_roots;
     uint64_t pool_bytes_max; /* cap on the BFS pool's device bytes; 0 = 1 GiB */
+    uint32_t flags;          /* GM_FLAG_* bits */
 } gm_run_opts;
 
 GM_API void gm_default_opts(gm_run_opts *o);

@@ -74,6 +74,10 @@ class Graph:
         L.check(L.lib().gm_graph_info(self._h, ctypes.byref(inf)))
         return {k: getattr(inf, k) for k, _ in inf._fields_}
 
+    def build_hubs(self, budget_bytes=64 << 20, min_degree=64, stream=None):
+        """Rebuild the hub adjacency index (budget 0 removes it)."""
+        L.check(L.lib().gm_graph_build_hubs(self._h, int(budget_bytes), int(min_degree), _stream_handle(stream)))
+
     def export(self):
         """(offs, nbr, labels) copied to host numpy arrays."""
         inf = self.info()
@@ -172,7 +176,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
-          time_limit_ms=0.0, roots=None, pool_bytes_max=0):
+          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -192,6 +196,8 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.num_roots = keep.size
     if pool_bytes_max:
         o.pool_bytes_max = int(pool_bytes_max)
+    if not set_count:
+        o.flags |= L.GM_FLAG_NO_SET_COUNT
     return o, keep
 
 

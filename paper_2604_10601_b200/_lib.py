@@ -18,11 +18,12 @@ LIB_PATH = os.path.join(_HERE, "libgmatch.so")
 GM_OK, GM_ERR_ARG, GM_ERR_CUDA, GM_ERR_NOMEM, GM_ERR_LIMIT, GM_TIMEOUT = 0, 1, 2, 3, 4, 5
 GM_MEM_HOST, GM_MEM_DEVICE = 0, 1
 GM_MAX_QUERY = 32
+GM_FLAG_NO_SET_COUNT = 1
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 
 # every symbol include/gmatch.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "gm_load_graph", "gm_graph_info", "gm_graph_export", "gm_free_graph",
+    "gm_load_graph", "gm_graph_info", "gm_graph_build_hubs", "gm_graph_export", "gm_free_graph",
     "gm_plan_query", "gm_plan_info", "gm_plan_candidates", "gm_free_plan",
     "gm_default_opts", "gm_count", "gm_enumerate", "gm_last_error", "gm_version",
 ]
@@ -30,7 +31,8 @@ EXPORTS = [
 
 class GraphInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_uint64), ("num_adj", ctypes.c_uint64), ("num_labels", ctypes.c_uint32),
-                ("d_max", ctypes.c_uint32), ("device_bytes", ctypes.c_uint64)]
+                ("d_max", ctypes.c_uint32), ("device_bytes", ctypes.c_uint64), ("hubs", ctypes.c_uint32),
+                ("hub_min_degree", ctypes.c_uint32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -43,7 +45,8 @@ class RunOpts(ctypes.Structure):
                 ("root_chunk", ctypes.c_uint32), ("steal", ctypes.c_uint32),
                 ("blocks_per_sm", ctypes.c_uint32), ("warps_per_block", ctypes.c_uint32),
                 ("time_limit_ms", ctypes.c_double), ("roots", ctypes.POINTER(ctypes.c_uint32)),
-                ("num_roots", ctypes.c_uint64), ("pool_bytes_max", ctypes.c_uint64)]
+                ("num_roots", ctypes.c_uint64), ("pool_bytes_max", ctypes.c_uint64),
+                ("flags", ctypes.c_uint32)]
 
 
 class RunStats(ctypes.Structure):
@@ -74,6 +77,7 @@ def lib():
                                     ctypes.POINTER(vp)]
         L.gm_graph_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]
         L.gm_graph_export.argtypes = [vp, vp, vp, vp]
+        L.gm_graph_build_hubs.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, vp]
         L.gm_free_graph.argtypes = [vp]
         L.gm_free_graph.restype = None
         L.gm_plan_query.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p, u32p, ctypes.c_uint32, vp,

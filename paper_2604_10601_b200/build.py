@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmatch.so")
-SOURCES = ["graph.cu", "plan.cu", "search.cu"]
+SOURCES = ["graph.cu", "hubs.cu", "plan.cu", "search.cu"]
 HEADERS = ["gm_internal.cuh", os.path.join("..", "..", "include", "gmatch.h")]
 
 NVCC_FLAGS = [

@@ -46,7 +46,20 @@ struct gm_graph {
     uint32_t *nbr = nullptr;   // nadj neighbour ids, ascending inside each row
     uint32_t *lab = nullptr;   // n vertex labels
     uint64_t bytes = 0;
+    // hub adjacency index (hubs.cu): for the highest-degree vertices, a bitmap of N(v)
+    uint32_t nhubs = 0;
+    uint32_t hub_min_degree = 0;
+    uint32_t hub_words = 0;        // ceil(n/32) words per hub bitmap
+    uint32_t *hub_id = nullptr;    // n entries: hub slot of v, or 0xffffffff
+    uint32_t *hub_bits = nullptr;  // nhubs * hub_words
 };
+
+namespace gm {
+int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, cudaStream_t st);
+void free_hubs(gm_graph *g);
+constexpr uint64_t kDefaultHubBudget = 64ull << 20;   // fits beside the graph in the 126 MB L2
+constexpr uint32_t kDefaultHubMinDegree = 64;
+}  // namespace gm
 
 // Query plan: matching order, backward sets, candidate bitmaps.
 struct gm_plan {

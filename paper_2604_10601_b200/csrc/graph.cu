@@ -186,13 +186,19 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
         STEP(cudaGetLastError());
         STEP(cudaMemcpyAsync(&g->dmax, d_dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         STEP(cudaStreamSynchronize(st));
-        g->bytes = sizeof(uint32_t) * (rows + 1 + (nsel ? nsel : 1) + (n ? n : 1));
+        cudaFree(k0); cudaFree(k1); cudaFree(tmp);   // release sort scratch before the hub index
+        k0 = k1 = nullptr; tmp = nullptr;
+        rc = build_hubs(g, kDefaultHubBudget, kDefaultHubMinDegree, st);
+        if (rc != GM_OK) goto cleanup;
+        g->bytes = sizeof(uint32_t) * (rows + 1 + (nsel ? nsel : 1) + (n ? n : 1)) +
+                   (g->nhubs ? 4ull * (n + (uint64_t)g->nhubs * g->hub_words) : 0);
     }
 cleanup:
 #undef STEP
     cudaFree(d_src); cudaFree(d_dst); cudaFree(k0); cudaFree(k1); cudaFree(tmp); cudaFree(d_bad);
     if (rc != GM_OK) {
         cudaFree(g->offs); cudaFree(g->nbr); cudaFree(g->lab);
+        free_hubs(g);
         delete g;
         return rc;
     }
@@ -207,6 +213,8 @@ extern "C" int gm_graph_info(const gm_graph *g, gm_graph_info_t *info) {
     info->num_labels = g->S;
     info->d_max = g->dmax;
     info->device_bytes = g->bytes;
+    info->hubs = g->nhubs;
+    info->hub_min_degree = g->hub_min_degree;
     return GM_OK;
 }
 
@@ -221,5 +229,6 @@ extern "C" int gm_graph_export(const gm_graph *g, uint32_t *offs_host, uint32_t 
 extern "C" void gm_free_graph(gm_graph *g) {
     if (!g) return;
     cudaFree(g->offs); cudaFree(g->nbr); cudaFree(g->lab);
+    free_hubs(g);
     delete g;
 }

@@ -75,6 +75,13 @@ struct SearchParams {
     uint32_t *q_items;          // q_cap * kItemWords
     unsigned long long *q_seq;  // q_cap per-slot sequence numbers (Vyukov bounded MPMC ring)
     unsigned long long q_cap;
+    const uint32_t *__restrict__ hub_id;    // n entries (or null: no hub index)
+    const uint32_t *__restrict__ hub_bits;  // hub bitmaps, hub_words words each
+    uint32_t hub_words;
+    uint32_t bulk_last;         // 1: count the last level by set counting (count_last)
+    uint32_t last_b;            // position of phi[last]'s single backward neighbour
+    uint32_t last_same;         // positions i < last, i != last_b, with L(phi[i]) == L(phi[last])
+    uint32_t last_adj;          // positions adjacent to phi[last_b] in Q
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     unsigned long long deadline_ns;  // 0 = no limit
@@ -107,6 +114,23 @@ __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint
     return (ld_nc(P.cand + P.candoff[l] + (v >> 5)) >> (v & 31)) & 1u;
 }
 
+// v in N_lab(w)?  (v is known to have label lab.)  Hub bitmap if w is a hub, else a
+// binary search of w's label-lab row.
+__device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t w, uint32_t lab, uint32_t v,
+                                         uint32_t &words) {
+    if (P.hub_id) {
+        const uint32_t h = ld_nc(P.hub_id + w);
+        ++words;
+        if (h != 0xffffffffu) {
+            ++words;
+            return (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+        }
+    }
+    const uint32_t row = w * P.S + lab;
+    words += 2;
+    return contains(P.nbr, ld_nc(P.offs + row), ld_nc(P.offs + row + 1), v, words);
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -120,6 +144,7 @@ struct WarpStack {
     uint32_t cl[D][32];   //                  its length
     uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
     uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
+    uint32_t chk[D][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
 };
@@ -155,24 +180,104 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 // Process (Alg. 2 lines 32-41, Erratum 1 read as "lanes without a task return false"):
 // candidate-filter bit, then one walk up the pid chain checking injectivity and, for each
 // backward neighbour other than the slice's source, adjacency by binary search.
+//
+// Called by all 32 lanes together (lanes without a task pass has = false) and written to
+// stay converged: the pid-chain walk has the same trip count in every lane, the checks
+// run in a uniform loop over the (uniform) number of backward neighbours, and the binary
+// searches step in lock-step until every lane is done (instead of per-lane early exits
+// that leave most of the warp idle; ncu measured 12 active lanes/warp before).
 template <int D>
-__device__ __forceinline__ bool process(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t v, uint32_t src,
-                                        uint32_t &words) {
-    if (!cand_bit(P, l, v, words)) return false;
-    const uint32_t bw = P.bw[l] & ~(1u << S.cs[l][src]);
+__device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
+                                        bool has, uint32_t lane, uint32_t &words) {
+    bool ok = has && cand_bit(P, l, v, words);
+    const uint32_t cs = has ? S.cs[l][src] : 0u;
+    const uint32_t chk = P.bw[l] & ~(1u << cs);
     const uint32_t lab = P.lab[l];
     uint32_t p = src;
-    for (int i = l - 1; i >= 0; --i) {
+    int k = 0;
+    for (int i = l - 1; i >= 0; --i) {              // injectivity + collect the checks
         const uint32_t w = S.v[i][p];
-        if (w == v) return false;
-        if ((bw >> i) & 1u) {
-            const uint32_t row = w * P.S + lab;
-            words += 2;
-            if (!contains(P.nbr, ld_nc(P.offs + row), ld_nc(P.offs + row + 1), v, words)) return false;
-        }
+        ok = ok && (w != v);
+        if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
         p = S.pid[i][p];
     }
-    return true;
+    const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
+    for (int c = 0; c < nchk; ++c) {
+        if (!__any_sync(FULL, ok)) break;
+        const uint32_t w = S.chk[c][lane];
+        bool need = ok;
+        if (ok && P.hub_id) {
+            const uint32_t h = ld_nc(P.hub_id + w);
+            ++words;
+            if (h != 0xffffffffu) {
+                ++words;
+                ok = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+                need = false;
+            }
+        }
+        uint32_t n = 0;
+        const uint32_t *base = P.nbr;
+        if (need) {
+            const uint32_t row = w * P.S + lab;
+            const uint32_t lo = ld_nc(P.offs + row);
+            n = ld_nc(P.offs + row + 1) - lo;
+            base += lo;
+            words += 2;
+        }
+        while (__any_sync(FULL, n > 1)) {           // lock-step branch-free lower bound
+            if (n > 1) {
+                const uint32_t half = n >> 1;
+                base = (ld_nc(base + half) <= v) ? base + half : base;
+                n -= half;
+                ++words;
+            }
+        }
+        if (need) {
+            ok = n == 1 && ld_nc(base) == v;
+            words += n;
+        }
+    }
+    return ok;
+}
+
+// Last-level set counting (count mode): when phi[last] has ONE
+// backward neighbour phi[b], the valid extensions of a partial match M of depth last are
+// exactly the vertices of N_{L(phi[last])}(M[b]) not already in M (adjacency is the only
+// edge constraint; the candidate filter is implied -- every such v completes an embedding,
+// so it passes any sound filter).  A mapped M[i] can lie in that slice only if
+// L(phi[i]) = L(phi[last]) (bitmask same_lab); it surely does if phi[i] ~ phi[b] in Q
+// (adj_b), else one binary search decides.  Cost O(|M|) instead of O(|slice|) tasks.
+// (l, v, src) is the task that just completed M at level l = last - 1.
+template <int D>
+__device__ __forceinline__ uint32_t count_last(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t v,
+                                               uint32_t src, uint32_t &words) {
+    const int b = (int)P.last_b;
+    const uint32_t lab = P.lab[l + 1];
+    uint32_t mb = v;                      // M[b]
+    if (b != l) {
+        uint32_t p = src;
+        for (int i = l - 1; i > b; --i) p = S.pid[i][p];
+        mb = S.v[b][p];
+    }
+    const uint32_t row = mb * P.S + lab;
+    const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
+    words += 2;
+    uint32_t cnt = hi - lo;
+    uint32_t same = P.last_same;          // positions i < last, i != b, with L(phi[i]) == lab
+    if (same) {
+        if ((same >> l) & 1u) {
+            if (((P.last_adj >> l) & 1u) || has_edge(P, mb, lab, v, words)) --cnt;
+        }
+        uint32_t p = src;
+        for (int i = l - 1; i >= 0 && (same & ((1u << (i + 1)) - 1)); --i) {
+            if ((same >> i) & 1u) {
+                const uint32_t w = S.v[i][p];
+                if (((P.last_adj >> i) & 1u) || has_edge(P, mb, lab, w, words)) --cnt;
+            }
+            p = S.pid[i][p];
+        }
+    }
+    return cnt;
 }
 
 // Walk the chain of (level, lane) and write the prefix M[0..level] into dst (by position).
@@ -188,7 +293,7 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // ------------------------------------------------------------------ DFS kernel
 
 template <int D, bool ENUM>
-__global__ void __launch_bounds__(128) k_dfs(const SearchParams P) {
+__global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     WarpStack<D> &S = reinterpret_cast<WarpStack<D> *>(smem_raw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;
@@ -387,7 +492,7 @@ __global__ void __launch_bounds__(128) k_dfs(const SearchParams P) {
             my_tasks += has;
 
             // ---- Process
-            const bool F = has && process<D>(P, S, l, v, src, wacc);
+            const bool F = process<D>(P, S, l, v, src, has, lane, wacc);
             my_words += wacc + (has ? 1u : 0u);
             wacc = 0;
             if (l == last) {
@@ -407,6 +512,13 @@ __global__ void __launch_bounds__(128) k_dfs(const SearchParams P) {
                     }
                 }
                 my_count += F;
+                __syncwarp();
+                continue;
+            }
+            if (!ENUM && P.bulk_last && l == last - 1) {
+                // last-level set counting: the extensions of this partial match are exactly the
+                // label-L(phi[last]) neighbours of its backward neighbour minus the mapped ones
+                if (F) my_count += count_last<D>(P, S, l, v, src, wacc);
                 __syncwarp();
                 continue;
             }
@@ -480,7 +592,7 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
                 const uint32_t mi = __shfl_sync(FULL, m, i);
                 const uint32_t loi = __shfl_sync(FULL, lo, i), hii = __shfl_sync(FULL, hi, i);
                 if (F && v == mi) F = false;
-                if (F && ((checks >> i) & 1u)) F = contains(P.nbr, loi, hii, v, scratch);
+                if (F && ((checks >> i) & 1u)) F = has_edge(P, mi, lab, v, scratch);
             }
             const uint32_t fm = __ballot_sync(FULL, F);
             if (MODE == 0) {
@@ -675,6 +787,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.candoff[l] = p->order[l] * p->words;
         P.col[l] = p->order[l];
     }
+    P.hub_id = g->nhubs ? g->hub_id : nullptr;
+    P.hub_bits = g->hub_bits;
+    P.hub_words = g->hub_words;
     if (!W.ctrl) GM_CK(cudaMalloc(&W.ctrl, sizeof(Ctrl)));
     GM_CK(cudaMemsetAsync(W.ctrl, 0, sizeof(Ctrl), st));
     P.ctrl = W.ctrl;
@@ -804,6 +919,18 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             ++launches;
         }
         P.deadline_ns = deadline;
+        {   // last-level set counting applies when phi[last] has exactly one backward neighbour
+            const uint32_t last = p->nq - 1, bwl = p->bw[last];
+            if (!enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && last >= 1 && __builtin_popcount(bwl) == 1) {
+                const uint32_t b = (uint32_t)__builtin_ctz(bwl);
+                P.bulk_last = 1;
+                P.last_b = b;
+                for (uint32_t i = 0; i < last; ++i) {
+                    if (i != b && p->qlab[p->order[i]] == p->qlab[p->order[last]]) P.last_same |= 1u << i;
+                    if ((p->qadj[p->order[b]] >> p->order[i]) & 1u) P.last_adj |= 1u << i;
+                }
+            }
+        }
         GM_CK(cudaEventRecord(d0e, st));
         const uint32_t nq = p->nq;
         if (nq <= 8)

@@ -1,0 +1,34 @@
+"""One DFS launch of a bench workload for ncu (no time limit: work bounded by a root sample).
+   python tools/profile_one.py QUERY_INDEX NROOTS [CONFIG] [TAU]"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+import gminputs as gi  # noqa: E402
+import paper_2604_10601_b200 as gm  # noqa: E402
+
+qi = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+nroots = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+cfgname = sys.argv[3] if len(sys.argv) > 3 else "rmat18"
+tau = int(float(sys.argv[4])) if len(sys.argv) > 4 else 1000000
+cfg = bench.CONFIGS[cfgname]
+n, s, d, lab = bench.make_graph_device(cfg)
+sh, dh, lh = (x.cpu().numpy().view(np.uint32) for x in (s, d, lab))
+off, nb = gi.simple_adjacency(n, sh, dh)
+qs = bench.build_queries(cfg, off, nb, lh)
+g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
+q = qs[qi]
+p = gm.gm_plan_query(g, q)
+u0 = p.info()["order"][0]
+cands = np.flatnonzero(p.candidates(u0))
+roots = np.random.default_rng(0).permutation(cands)[:nroots].astype(np.uint32) if nroots > 0 else None
+for it in range(2):
+    t = time.time()
+    c, st = gm.gm_count(p, roots=roots, tau=tau)
+    print(q.name, len(q.edges), c, f"wall {time.time() - t:.3f}s",
+          {k: st[k] for k in ("dfs_ms", "total_ms", "tasks", "words", "pool_size", "pool_depth", "donations",
+                              "grid", "block")}, flush=True)
