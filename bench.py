@@ -255,6 +255,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     import gminputs as gi
     import paper_2604_10601_b200 as gm
+    from paper_2604_10601_b200 import partition
 
     # ---- inputs: graph generated on this GPU (replica per rank); queries from host adjacency
     n, s_dev, d_dev, lab_dev = make_graph_device(cfg)
@@ -284,8 +285,7 @@ def main():
             e1.record(stream)
             plans.append(p)
             out.append((st, e0, e1))
-        if world > 1:
-            dist.all_reduce(counts_dev)          # the one collective of the step
+        partition.reduce_counts(counts_dev)      # the one collective of the step (N > 1)
         return out, plans
 
     for _ in range(args.warmup):

@@ -170,8 +170,9 @@ typedef struct {
     uint32_t blocks_per_sm;  /* 0 = as many as fit */
     uint32_t warps_per_block;/* 0 = 4 */
     double   time_limit_ms;  /* 0 = none; on expiry the call returns GM_TIMEOUT */
-    const uint32_t *roots;   /* optional host list restricting phi[0]'s images to
-                                these vertices (still filtered and rank-partitioned) */
+    const uint32_t *roots;   /* optional host list of DISTINCT vertices restricting phi[0]'s
+                                images to them (still filtered and rank-partitioned);
+                                non-NULL with num_roots = 0 means no roots (count 0) */
     uint64_t num_roots;
     uint64_t pool_bytes_max; /* cap on the BFS pool's device bytes; 0 = 1 GiB */
     uint32_t flags;          /* GM_FLAG_* bits */

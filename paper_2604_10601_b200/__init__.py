@@ -191,9 +191,11 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
     o.time_limit_ms = float(time_limit_ms)
     keep = None
     if roots is not None:
-        keep = np.ascontiguousarray(np.asarray(roots, dtype=np.uint32))
+        r = np.asarray(roots, dtype=np.uint32).reshape(-1)
+        keep = np.zeros(max(1, r.size), dtype=np.uint32)   # never a NULL pointer, even when empty
+        keep[: r.size] = r
         o.roots = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
-        o.num_roots = keep.size
+        o.num_roots = r.size
     if pool_bytes_max:
         o.pool_bytes_max = int(pool_bytes_max)
     if not set_count:

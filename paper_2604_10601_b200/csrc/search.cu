@@ -202,40 +202,63 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         p = S.pid[i][p];
     }
     const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
-    for (int c = 0; c < nchk; ++c) {
+    // Two checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
+    // independent, so each lane keeps two dependent-load chains in flight (ncu: the kernel
+    // is bound by long-scoreboard stalls on L2-resident probes, not by bandwidth).
+    for (int c = 0; c < nchk; c += 2) {
         if (!__any_sync(FULL, ok)) break;
-        const uint32_t w = S.chk[c][lane];
-        bool need = ok;
+        const bool two = c + 1 < nchk;
+        const uint32_t w0 = S.chk[c][lane];
+        const uint32_t w1 = two ? S.chk[c + 1][lane] : 0u;
+        uint32_t h0 = 0xffffffffu, h1 = 0xffffffffu;
         if (ok && P.hub_id) {
-            const uint32_t h = ld_nc(P.hub_id + w);
-            ++words;
-            if (h != 0xffffffffu) {
+            h0 = ld_nc(P.hub_id + w0);
+            if (two) h1 = ld_nc(P.hub_id + w1);
+            words += two ? 2u : 1u;
+        }
+        bool r0 = true, r1 = true, need0 = false, need1 = false;
+        uint32_t b0 = 0, n0 = 0, b1 = 0, n1 = 0;
+        if (ok) {
+            if (h0 != 0xffffffffu) {
+                r0 = (ld_nc(P.hub_bits + (unsigned long long)h0 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
                 ++words;
-                ok = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
-                need = false;
+            } else {
+                const uint32_t row = w0 * P.S + lab;
+                b0 = ld_nc(P.offs + row);
+                n0 = ld_nc(P.offs + row + 1) - b0;
+                need0 = true;
+                words += 2;
+            }
+            if (two) {
+                if (h1 != 0xffffffffu) {
+                    r1 = (ld_nc(P.hub_bits + (unsigned long long)h1 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+                    ++words;
+                } else {
+                    const uint32_t row = w1 * P.S + lab;
+                    b1 = ld_nc(P.offs + row);
+                    n1 = ld_nc(P.offs + row + 1) - b1;
+                    need1 = true;
+                    words += 2;
+                }
             }
         }
-        uint32_t n = 0;
-        const uint32_t *base = P.nbr;
-        if (need) {
-            const uint32_t row = w * P.S + lab;
-            const uint32_t lo = ld_nc(P.offs + row);
-            n = ld_nc(P.offs + row + 1) - lo;
-            base += lo;
-            words += 2;
-        }
-        while (__any_sync(FULL, n > 1)) {           // lock-step branch-free lower bound
-            if (n > 1) {
-                const uint32_t half = n >> 1;
-                base = (ld_nc(base + half) <= v) ? base + half : base;
-                n -= half;
+        while (__any_sync(FULL, n0 > 1 || n1 > 1)) {   // lock-step branch-free lower bounds
+            if (n0 > 1) {
+                const uint32_t half = n0 >> 1;
+                b0 = (ld_nc(P.nbr + b0 + half) <= v) ? b0 + half : b0;
+                n0 -= half;
+                ++words;
+            }
+            if (n1 > 1) {
+                const uint32_t half = n1 >> 1;
+                b1 = (ld_nc(P.nbr + b1 + half) <= v) ? b1 + half : b1;
+                n1 -= half;
                 ++words;
             }
         }
-        if (need) {
-            ok = n == 1 && ld_nc(base) == v;
-            words += n;
-        }
+        if (need0) { r0 = n0 == 1 && ld_nc(P.nbr + b0) == v; words += n0; }
+        if (need1) { r1 = n1 == 1 && ld_nc(P.nbr + b1) == v; words += n1; }
+        ok = ok && r0 && r1;
     }
     return ok;
 }
@@ -798,7 +821,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
 
     // ---- root candidates (rank share)
     uint32_t *d_user = nullptr;
-    const unsigned long long nroot_cap = o.num_roots ? o.num_roots : g->n;
+    // a non-NULL root list restricts phi[0]'s images to it (an empty list: no embeddings)
+    const unsigned long long nroot_cap = o.roots ? o.num_roots : g->n;
     int rc = ensure(W.buf[0], W.buf_bytes[0], sizeof(uint32_t) * (nroot_cap ? nroot_cap : 1));
     if (rc) return rc;
     if (o.num_roots) {

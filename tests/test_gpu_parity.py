@@ -332,30 +332,68 @@ def test_config2_sampled_roots(gm):
     GPU count restricted to sampled roots == sum of the oracle's per-root counts.  Roots are
     sampled among phi[0]'s candidates whose oracle count stays under a budget (the oracle
     must finish); the GPU runs in the bench launch configuration (tau = 1e6, stealing on)."""
-    n, s, d = gi.rmat_edges(18, 16, 2)
-    lab = gi.uniform_labels(n, 8, 2)
+    import bench
+    cfg = bench.CONFIGS["rmat18"]
+    n, s, d, lab = bench.make_graph_host(cfg)
     off, nb = gi.simple_adjacency(n, s, d)
-    g = gm.gm_load_graph(n, s, d, lab, 8)
+    queries = bench.build_queries(cfg, off, nb, lab)          # the bench's query set
+    g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
     og = OracleGraph(n, s, d, lab)
     rs = np.random.default_rng(1)
-    budget = 300_000            # oracle search-tree nodes per sampled root
-    checked = 0
-    for qs in range(4):
-        q = (gi.random_query if qs % 2 == 0 else gi.random_walk_query)(off, nb, lab, 8, seed=100 + qs)
+    budget = 100_000            # oracle search-tree nodes per sampled root
+    checked, nonzero = 0, 0
+    for q in queries:
         p = gm.gm_plan_query(g, q)
         u0 = p.info()["order"][0]
         cands = np.flatnonzero(p.candidates(u0))
         roots, ref = [], 0
-        for v in rs.permutation(cands)[:40]:
+        for v in rs.permutation(cands)[:300]:
             c = og.count(q, fixed=(u0, int(v)), max_nodes=budget)
             if c is not None:
                 roots.append(int(v)); ref += c
-            if len(roots) == 8:
+                nonzero += c > 0
+            if len(roots) == 6:
                 break
-        c, _ = gm.gm_count(p, roots=np.array(roots, np.uint32))
+        c, st = gm.gm_count(p, roots=np.array(roots, np.uint32), time_limit_ms=60000)
+        assert st["timed_out"] == 0
         assert c == ref, (q, roots)
         checked += len(roots)
-    assert checked >= 8
+        # the 5-vertex prefix of the planner's order (an induced, connected sub-query) has
+        # per-root counts the oracle finishes: exact parity on sampled roots
+        order = p.info()["order"][:5]
+        idx = {u: i for i, u in enumerate(order)}
+        sub = gi.Query(5, [(idx[a], idx[b]) for a, b in q.edges.tolist() if a in idx and b in idx],
+                       [int(q.labels[u]) for u in order])
+        ps = gm.gm_plan_query(g, sub)
+        s0 = ps.info()["order"][0]
+        sroots, sref = [], 0
+        for v in rs.permutation(np.flatnonzero(ps.candidates(s0)))[:100]:
+            cc = og.count(sub, fixed=(s0, int(v)), max_nodes=1_000_000)
+            if cc is not None:
+                sroots.append(int(v)); sref += cc
+                nonzero += cc > 0
+            if len(sroots) == 6:
+                break
+        assert gm.gm_count(ps, roots=np.array(sroots, np.uint32))[0] == sref
+        checked += len(sroots)
+    assert checked >= 24 and nonzero >= 8
+    # an explicit empty root list means no roots at all
+    p = gm.gm_plan_query(g, queries[0])
+    assert gm.gm_count(p, roots=np.zeros(0, np.uint32))[0] == 0
+    # full queries at full size through gm_enumerate: every listed row is a distinct embedding
+    off_o, adj_o = og.csr()
+    for q in queries:
+        p = gm.gm_plan_query(g, q)
+        rows, total, st = gm.gm_enumerate(p, capacity=4096, time_limit_ms=300)
+        assert len(rows) == min(4096, total) and len(rows) > 0
+        assert len({tuple(r) for r in rows.tolist()}) == len(rows)
+        for r in rows[:512].astype(np.int64):
+            assert len(set(r.tolist())) == q.n                              # injective
+            assert np.array_equal(lab[r], q.labels)                         # labels
+            for a, b in q.edges.tolist():                                   # edges
+                nb_a = adj_o[off_o[r[a]]:off_o[r[a] + 1]]
+                i = np.searchsorted(nb_a, r[b])
+                assert i < len(nb_a) and nb_a[i] == r[b]
 
 
 @pytest.mark.parametrize("seed", range(6))
