@@ -45,6 +45,8 @@ def _load():
                                  ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, _u32p, ctypes.c_uint64]
         lib.or_count_budget.restype = ctypes.c_uint64
         lib.or_count_budget.argtypes = lib.or_count.argtypes + [ctypes.c_uint64]
+        lib.or_last_found.restype = ctypes.c_uint64
+        lib.or_last_found.argtypes = []
         lib.or_filter.restype = ctypes.c_int
         lib.or_filter.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _u32p, _u32p,
                                   ctypes.c_int, ctypes.c_uint32, _u8p]
@@ -95,6 +97,12 @@ class OracleGraph:
         if r == 2 ** 64 - 2:
             return None
         return int(r)
+
+    def count_budgeted(self, q, fixed=None, max_nodes=1_000_000):
+        """(embeddings found, complete) after at most max_nodes search-tree nodes.  For timing
+        the oracle on bounded work (bench.py cpu_baseline); not an expected value."""
+        r = self.count(q, fixed=fixed, max_nodes=max_nodes)
+        return int(_load().or_last_found()), r is not None
 
     def enumerate(self, q, fixed=None, cap=None) -> np.ndarray:
         """All embeddings as an (count, nq) array, rows sorted lexicographically."""

@@ -101,6 +101,12 @@ static int has_edge(const or_graph *g, uint32_t a, uint32_t b) {
 
 /* ---------------------------------------------------------------- matcher */
 
+/* Embeddings found by the last or_count/or_count_budget call on this thread, including a
+ * call whose node budget ran out (then a lower bound) -- lets bench.py time the oracle on
+ * a bounded amount of search work.  Never used as an expected value. */
+static _Thread_local uint64_t g_last_found;
+uint64_t or_last_found(void) { return g_last_found; }
+
 typedef struct {
     const or_graph *g;
     int nq;
@@ -222,6 +228,7 @@ uint64_t or_count_budget(const or_graph *g, int nq, int mq, const uint32_t *qedg
     }
     c->used = (uint8_t *)calloc((size_t)g->n + 1, 1);
     search(c, 0);
+    g_last_found = c->count;
     uint64_t r = (c->max_nodes && c->nodes > c->max_nodes) ? UINT64_MAX - 1 : c->count;
     free(c->used); free(c);
     return r;
