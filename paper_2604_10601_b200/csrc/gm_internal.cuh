@@ -46,11 +46,14 @@ struct gm_graph {
     uint32_t *nbr = nullptr;   // nadj neighbour ids, ascending inside each row
     uint32_t *lab = nullptr;   // n vertex labels
     uint64_t bytes = 0;
-    // hub adjacency index (hubs.cu): for the highest-degree vertices, a bitmap of N(v)
+    // vertex renumbering by decreasing degree (graph.cu): device ids are new ids
+    uint32_t *old2new = nullptr;   // n: original id -> device id
+    uint32_t *new2old = nullptr;   // n: device id -> original id
+    // hub adjacency index (hubs.cu): device ids 0..nhubs-1 (the highest-degree vertices)
+    // each have a bitmap of N(v) over device ids, row v of hub_bits
     uint32_t nhubs = 0;
     uint32_t hub_min_degree = 0;
     uint32_t hub_words = 0;        // ceil(n/32) words per hub bitmap
-    uint32_t *hub_id = nullptr;    // n entries: hub slot of v, or 0xffffffff
     uint32_t *hub_bits = nullptr;  // nhubs * hub_words
 };
 

@@ -1,15 +1,23 @@
-// graph.cu -- gm_load_graph: edge list -> label-partitioned CSR in HBM.
+// graph.cu -- gm_load_graph: edge list -> degree-ordered, label-partitioned CSR in HBM.
 //
 // PAPER.md §2.1 (lines 143-147): G is an undirected, labelled, simple graph;
-// N(v) is the neighbour set.  The device layout stores,
-// for row r = v*S + l, the neighbours of v whose label is l, ascending:
-//     nbr[offs[r] .. offs[r+1])
-// so N(v) restricted to label l -- the only part of N(v) that can hold candidates
-// of a query vertex with label l -- is one contiguous, sorted slice.  The build is
-// one radix sort of 64-bit keys (row << 32 | neighbour) of both edge directions,
-// a dedup, and an offsets pass.
+// N(v) is the neighbour set.  The device layout:
+//   * vertices are renumbered by decreasing degree (ties by original id), so the
+//     highest-degree vertices -- the hubs of a power-law graph -- are ids 0..K-1: "w is a
+//     hub" is the compare w < K and a hub's bitmap row is row w (hubs.cu).  The API speaks
+//     original ids: old2new / new2old map at the boundary (roots in, embeddings out,
+//     exports), never inside the search.
+//   * for row r = v*S + l (v a new id), nbr[offs[r] .. offs[r+1]) holds the neighbours of v
+//     whose label is l, ascending, so N(v) restricted to label l -- the only part of N(v)
+//     that can hold candidates of a query vertex with label l -- is one sorted slice.
+// The build: degree histogram + one sort of vertices, then one radix sort of 64-bit keys
+// (row << 32 | neighbour) of both edge directions, a dedup, and an offsets pass.
 #include <cub/cub.cuh>
 #include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
 
 #include "gm_internal.cuh"
 
@@ -24,19 +32,31 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 
-// Directed keys for both orientations; self loops become the max sentinel.
-__global__ void k_make_keys(uint64_t m, const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                            const uint32_t *__restrict__ lab, uint32_t S, uint64_t n,
-                            unsigned long long *__restrict__ keys, int *__restrict__ bad) {
-    const unsigned long long sentinel = (unsigned long long)(n * S) << 32;  // row past the last
+// Approximate degrees (repeated pairs counted twice; self loops skipped) and id validity.
+__global__ void k_degree_count(uint64_t m, const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                               uint64_t n, uint32_t *__restrict__ deg, int *__restrict__ bad) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t a = src[i], b = dst[i];
-        if (a >= n || b >= n) { *bad = 1; keys[2 * i] = keys[2 * i + 1] = sentinel; continue; }
-        if (a == b) { keys[2 * i] = keys[2 * i + 1] = sentinel; continue; }
-        uint32_t la = lab ? lab[a] : 0, lb = lab ? lab[b] : 0;
-        keys[2 * i] = ((unsigned long long)((uint64_t)a * S + lb) << 32) | b;
-        keys[2 * i + 1] = ((unsigned long long)((uint64_t)b * S + la) << 32) | a;
+        const uint32_t a = src[i], b = dst[i];
+        if (a >= n || b >= n) { *bad = 1; continue; }
+        if (a == b) continue;
+        atomicAdd(deg + a, 1u);
+        atomicAdd(deg + b, 1u);
+    }
+}
+
+__global__ void k_iota(uint64_t n, uint32_t *__restrict__ ids) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+        ids[v] = (uint32_t)v;
+}
+
+// old2new = inverse of new2old; labels permuted into the new id order.
+__global__ void k_renumber(uint64_t n, const uint32_t *__restrict__ new2old, const uint32_t *__restrict__ lab_in,
+                           uint32_t *__restrict__ old2new, uint32_t *__restrict__ lab_out) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t o = new2old[v];
+        old2new[o] = (uint32_t)v;
+        lab_out[v] = lab_in ? lab_in[o] : 0;
     }
 }
 
@@ -44,6 +64,21 @@ __global__ void k_check_labels(uint64_t n, const uint32_t *__restrict__ lab, uin
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         if (lab[i] >= S) *bad = 1;
+}
+
+// Directed keys (new ids) for both orientations; self loops become a sentinel row.
+__global__ void k_make_keys(uint64_t m, const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                            const uint32_t *__restrict__ old2new, const uint32_t *__restrict__ lab, uint32_t S,
+                            uint64_t n, unsigned long long *__restrict__ keys) {
+    const unsigned long long sentinel = (unsigned long long)(n * S) << 32;  // row past the last
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a0 = src[i], b0 = dst[i];
+        if (a0 >= n || b0 >= n || a0 == b0) { keys[2 * i] = keys[2 * i + 1] = sentinel; continue; }
+        const uint32_t a = old2new[a0], b = old2new[b0];
+        keys[2 * i] = ((unsigned long long)((uint64_t)a * S + lab[b]) << 32) | b;
+        keys[2 * i + 1] = ((unsigned long long)((uint64_t)b * S + lab[a]) << 32) | a;
+    }
 }
 
 // offs[r] = first position whose row >= r.  Each position that starts a new row
@@ -79,7 +114,7 @@ static int grid_for(uint64_t work, int block = 256) {
 using namespace gm;
 
 extern "C" const char *gm_last_error(void) { return g_err; }
-extern "C" const char *gm_version(void) { return "gmatch-b200 0.1 (sm_100a)"; }
+extern "C" const char *gm_version(void) { return "gmatch-b200 0.2 (sm_100a)"; }
 
 extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const uint32_t *dst,
                              const uint32_t *labels, uint32_t num_labels, int mem, void *stream_,
@@ -98,12 +133,14 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
     cudaStream_t st = (cudaStream_t)stream_;
     const uint32_t S = num_labels;
     const uint64_t rows = n * S;
+    const uint64_t nn = n ? n : 1;
 
     gm_graph *g = new gm_graph();
     GM_CK(cudaGetDevice(&g->device));
     g->n = n; g->S = S;
 
-    uint32_t *d_src = nullptr, *d_dst = nullptr;
+    uint32_t *d_src = nullptr, *d_dst = nullptr, *lab_in = nullptr;
+    uint32_t *deg = nullptr, *deg_s = nullptr, *ids = nullptr;
     unsigned long long *k0 = nullptr, *k1 = nullptr;
     void *tmp = nullptr;
     int *d_bad = nullptr;
@@ -120,8 +157,11 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
         }                                                                                  \
     } while (0)
     {
-        const uint32_t *s = src, *d = dst, *l = labels;
-        STEP(cudaMalloc(&g->lab, sizeof(uint32_t) * (n ? n : 1)));
+        const uint32_t *s = src, *d = dst;
+        STEP(cudaMalloc(&g->lab, sizeof(uint32_t) * nn));
+        STEP(cudaMalloc(&g->old2new, sizeof(uint32_t) * nn));
+        STEP(cudaMalloc(&g->new2old, sizeof(uint32_t) * nn));
+        if (labels) STEP(cudaMalloc(&lab_in, sizeof(uint32_t) * nn));
         if (mem == GM_MEM_HOST) {
             if (m) {
                 STEP(cudaMalloc(&d_src, sizeof(uint32_t) * m));
@@ -130,24 +170,39 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
                 STEP(cudaMemcpyAsync(d_dst, dst, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
             }
             s = d_src; d = d_dst;
-            if (labels) {
-                STEP(cudaMemcpyAsync(g->lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
-            }
-        } else if (labels) {
-            STEP(cudaMemcpyAsync(g->lab, labels, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
+            if (labels && n) STEP(cudaMemcpyAsync(lab_in, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+        } else if (labels && n) {
+            STEP(cudaMemcpyAsync(lab_in, labels, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
         }
-        if (!labels) STEP(cudaMemsetAsync(g->lab, 0, sizeof(uint32_t) * (n ? n : 1), st));
-        l = g->lab;
 
         STEP(cudaMalloc(&d_bad, 4 * sizeof(int)));
         STEP(cudaMemsetAsync(d_bad, 0, 4 * sizeof(int), st));
         d_nsel = (unsigned long long *)(d_bad + 2);
-        if (n) k_check_labels<<<grid_for(n), 256, 0, st>>>(n, l, S, d_bad);
+        if (labels && n) k_check_labels<<<grid_for(n), 256, 0, st>>>(n, lab_in, S, d_bad);
 
+        // ---- degree order: new id = rank of the vertex by (approximate degree desc, id asc)
+        STEP(cudaMalloc(&deg, sizeof(uint32_t) * nn));
+        STEP(cudaMalloc(&deg_s, sizeof(uint32_t) * nn));
+        STEP(cudaMalloc(&ids, sizeof(uint32_t) * nn));
+        STEP(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * nn, st));
+        if (m) k_degree_count<<<grid_for(m), 256, 0, st>>>(m, s, d, n, deg, d_bad);
+        if (n) k_iota<<<grid_for(n), 256, 0, st>>>(n, ids);
+        if (n) {
+            size_t tbs = 0;
+            STEP(cub::DeviceRadixSort::SortPairsDescending(nullptr, tbs, deg, deg_s, ids, g->new2old, (int64_t)n, 0, 32, st));
+            STEP(cudaMalloc(&tmp, tbs ? tbs : 16));
+            STEP(cub::DeviceRadixSort::SortPairsDescending(tmp, tbs, deg, deg_s, ids, g->new2old, (int64_t)n, 0, 32, st));
+            STEP(cudaFree(tmp));
+            tmp = nullptr;
+            k_renumber<<<grid_for(n), 256, 0, st>>>(n, g->new2old, lab_in, g->old2new, g->lab);
+        }
+        STEP(cudaGetLastError());
+
+        // ---- adjacency keys, sort, dedup, offsets
         const uint64_t K = 2 * m;
         STEP(cudaMalloc(&k0, sizeof(unsigned long long) * (K ? K : 1)));
         STEP(cudaMalloc(&k1, sizeof(unsigned long long) * (K ? K : 1)));
-        if (m) k_make_keys<<<grid_for(m), 256, 0, st>>>(m, s, d, l, S, n, k0, d_bad);
+        if (m) k_make_keys<<<grid_for(m), 256, 0, st>>>(m, s, d, g->old2new, g->lab, S, n, k0);
         STEP(cudaGetLastError());
 
         int end_bit = 32;  // keys are (row << 32 | nbr) with row <= rows (sentinel = rows)
@@ -190,14 +245,15 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
         k0 = k1 = nullptr; tmp = nullptr;
         rc = build_hubs(g, kDefaultHubBudget, kDefaultHubMinDegree, st);
         if (rc != GM_OK) goto cleanup;
-        g->bytes = sizeof(uint32_t) * (rows + 1 + (nsel ? nsel : 1) + (n ? n : 1)) +
-                   (g->nhubs ? 4ull * (n + (uint64_t)g->nhubs * g->hub_words) : 0);
+        g->bytes = sizeof(uint32_t) * (rows + 1 + (nsel ? nsel : 1) + 3 * nn) +
+                   4ull * (uint64_t)g->nhubs * g->hub_words;
     }
 cleanup:
 #undef STEP
-    cudaFree(d_src); cudaFree(d_dst); cudaFree(k0); cudaFree(k1); cudaFree(tmp); cudaFree(d_bad);
+    cudaFree(d_src); cudaFree(d_dst); cudaFree(lab_in); cudaFree(deg); cudaFree(deg_s); cudaFree(ids);
+    cudaFree(k0); cudaFree(k1); cudaFree(tmp); cudaFree(d_bad);
     if (rc != GM_OK) {
-        cudaFree(g->offs); cudaFree(g->nbr); cudaFree(g->lab);
+        cudaFree(g->offs); cudaFree(g->nbr); cudaFree(g->lab); cudaFree(g->old2new); cudaFree(g->new2old);
         free_hubs(g);
         delete g;
         return rc;
@@ -218,17 +274,43 @@ extern "C" int gm_graph_info(const gm_graph *g, gm_graph_info_t *info) {
     return GM_OK;
 }
 
+// Export in ORIGINAL ids: row v*S + l = original ids of v's label-l neighbours, ascending.
 extern "C" int gm_graph_export(const gm_graph *g, uint32_t *offs_host, uint32_t *nbr_host, uint32_t *labels_host) {
     GM_REQ(g, GM_ERR_ARG, "gm_graph_export: NULL graph");
-    if (offs_host) GM_CK(cudaMemcpy(offs_host, g->offs, sizeof(uint32_t) * (g->n * g->S + 1), cudaMemcpyDeviceToHost));
-    if (nbr_host && g->nadj) GM_CK(cudaMemcpy(nbr_host, g->nbr, sizeof(uint32_t) * g->nadj, cudaMemcpyDeviceToHost));
-    if (labels_host && g->n) GM_CK(cudaMemcpy(labels_host, g->lab, sizeof(uint32_t) * g->n, cudaMemcpyDeviceToHost));
+    const uint64_t n = g->n, S = g->S, rows = n * S;
+    std::vector<uint32_t> offs(rows + 1), nbr(g->nadj), lab(n), n2o(n), o2n(n);
+    GM_CK(cudaMemcpy(offs.data(), g->offs, sizeof(uint32_t) * (rows + 1), cudaMemcpyDeviceToHost));
+    if (g->nadj) GM_CK(cudaMemcpy(nbr.data(), g->nbr, sizeof(uint32_t) * g->nadj, cudaMemcpyDeviceToHost));
+    if (n) {
+        GM_CK(cudaMemcpy(lab.data(), g->lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+        GM_CK(cudaMemcpy(n2o.data(), g->new2old, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+        GM_CK(cudaMemcpy(o2n.data(), g->old2new, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    }
+    if (labels_host)
+        for (uint64_t v = 0; v < n; ++v) labels_host[v] = lab[o2n[v]];
+    if (offs_host || nbr_host) {
+        uint64_t pos = 0;
+        std::vector<uint32_t> row;
+        for (uint64_t v = 0; v < n; ++v) {
+            const uint64_t nv = o2n[v];
+            for (uint64_t l = 0; l < S; ++l) {
+                if (offs_host) offs_host[v * S + l] = (uint32_t)pos;
+                const uint64_t r = nv * S + l;
+                row.assign(nbr.begin() + offs[r], nbr.begin() + offs[r + 1]);
+                for (auto &w : row) w = n2o[w];
+                std::sort(row.begin(), row.end());
+                if (nbr_host) std::copy(row.begin(), row.end(), nbr_host + pos);
+                pos += row.size();
+            }
+        }
+        if (offs_host) offs_host[rows] = (uint32_t)pos;
+    }
     return GM_OK;
 }
 
 extern "C" void gm_free_graph(gm_graph *g) {
     if (!g) return;
-    cudaFree(g->offs); cudaFree(g->nbr); cudaFree(g->lab);
+    cudaFree(g->offs); cudaFree(g->nbr); cudaFree(g->lab); cudaFree(g->old2new); cudaFree(g->new2old);
     free_hubs(g);
     delete g;
 }

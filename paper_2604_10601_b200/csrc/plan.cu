@@ -254,9 +254,16 @@ extern "C" int gm_plan_info(const gm_plan *p, gm_plan_info_t *info) {
 extern "C" int gm_plan_candidates(const gm_plan *p, uint32_t u, uint32_t *words_host) {
     GM_REQ(p && words_host, GM_ERR_ARG, "gm_plan_candidates: NULL argument");
     GM_REQ(u < p->nq, GM_ERR_ARG, "gm_plan_candidates: u=%u >= nq", u);
-    if (p->words)
-        GM_CK(cudaMemcpy(words_host, p->cand + (uint64_t)u * p->words, sizeof(uint32_t) * p->words,
-                         cudaMemcpyDeviceToHost));
+    if (!p->words) return GM_OK;
+    // the bitmap is over device ids; report it over the caller's (original) ids
+    const uint64_t n = p->g->n;
+    std::vector<uint32_t> dev(p->words), n2o(n);
+    GM_CK(cudaMemcpy(dev.data(), p->cand + (uint64_t)u * p->words, sizeof(uint32_t) * p->words,
+                     cudaMemcpyDeviceToHost));
+    GM_CK(cudaMemcpy(n2o.data(), p->g->new2old, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    memset(words_host, 0, sizeof(uint32_t) * p->words);
+    for (uint64_t v = 0; v < n; ++v)
+        if ((dev[v >> 5] >> (v & 31)) & 1u) words_host[n2o[v] >> 5] |= 1u << (n2o[v] & 31);
     return GM_OK;
 }
 

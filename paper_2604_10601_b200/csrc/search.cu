@@ -75,9 +75,11 @@ struct SearchParams {
     uint32_t *q_items;          // q_cap * kItemWords
     unsigned long long *q_seq;  // q_cap per-slot sequence numbers (Vyukov bounded MPMC ring)
     unsigned long long q_cap;
-    const uint32_t *__restrict__ hub_id;    // n entries (or null: no hub index)
-    const uint32_t *__restrict__ hub_bits;  // hub bitmaps, hub_words words each
+    const uint32_t *__restrict__ hub_bits;  // hub bitmaps (row w for device ids w < nhubs)
+    uint32_t nhubs;                         // 0: no hub index
     uint32_t hub_words;
+    const uint32_t *__restrict__ new2old;   // device id -> original id (enumerate output)
+    const uint32_t *__restrict__ old2new;   // original id -> device id (user roots)
     uint32_t bulk_last;         // 1: count the last level by set counting (count_last)
     uint32_t last_b;            // position of phi[last]'s single backward neighbour
     uint32_t last_same;         // positions i < last, i != last_b, with L(phi[i]) == L(phi[last])
@@ -114,17 +116,13 @@ __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint
     return (ld_nc(P.cand + P.candoff[l] + (v >> 5)) >> (v & 31)) & 1u;
 }
 
-// v in N_lab(w)?  (v is known to have label lab.)  Hub bitmap if w is a hub, else a
-// binary search of w's label-lab row.
+// v in N_lab(w)?  (v is known to have label lab.)  Hub bitmap if w is a hub (w < nhubs:
+// device ids are ordered by degree), else a binary search of w's label-lab row.
 __device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t w, uint32_t lab, uint32_t v,
                                          uint32_t &words) {
-    if (P.hub_id) {
-        const uint32_t h = ld_nc(P.hub_id + w);
+    if (w < P.nhubs) {
         ++words;
-        if (h != 0xffffffffu) {
-            ++words;
-            return (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
-        }
+        return (ld_nc(P.hub_bits + (unsigned long long)w * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
     }
     const uint32_t row = w * P.S + lab;
     words += 2;
@@ -210,17 +208,11 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         const bool two = c + 1 < nchk;
         const uint32_t w0 = S.chk[c][lane];
         const uint32_t w1 = two ? S.chk[c + 1][lane] : 0u;
-        uint32_t h0 = 0xffffffffu, h1 = 0xffffffffu;
-        if (ok && P.hub_id) {
-            h0 = ld_nc(P.hub_id + w0);
-            if (two) h1 = ld_nc(P.hub_id + w1);
-            words += two ? 2u : 1u;
-        }
         bool r0 = true, r1 = true, need0 = false, need1 = false;
         uint32_t b0 = 0, n0 = 0, b1 = 0, n1 = 0;
         if (ok) {
-            if (h0 != 0xffffffffu) {
-                r0 = (ld_nc(P.hub_bits + (unsigned long long)h0 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+            if (w0 < P.nhubs) {
+                r0 = (ld_nc(P.hub_bits + (unsigned long long)w0 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
                 ++words;
             } else {
                 const uint32_t row = w0 * P.S + lab;
@@ -230,8 +222,8 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
                 words += 2;
             }
             if (two) {
-                if (h1 != 0xffffffffu) {
-                    r1 = (ld_nc(P.hub_bits + (unsigned long long)h1 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+                if (w1 < P.nhubs) {
+                    r1 = (ld_nc(P.hub_bits + (unsigned long long)w1 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
                     ++words;
                 } else {
                     const uint32_t row = w1 * P.S + lab;
@@ -528,9 +520,12 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
                         const unsigned long long idx = basepos + __popc(fm & ((1u << lane) - 1));
                         if (idx < P.out_cap) {
                             uint32_t *row = P.out + idx * P.nq;
-                            row[P.col[l]] = v;
+                            row[P.col[l]] = ld_nc(P.new2old + v);        // original ids out
                             uint32_t p = src;
-                            for (int i = l - 1; i >= 0; --i) { row[P.col[i]] = S.v[i][p]; p = S.pid[i][p]; }
+                            for (int i = l - 1; i >= 0; --i) {
+                                row[P.col[i]] = ld_nc(P.new2old + S.v[i][p]);
+                                p = S.pid[i][p];
+                            }
                         }
                     }
                 }
@@ -630,12 +625,12 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
                     const uint32_t mi = __shfl_sync(FULL, m, i);
                     if (wr) {
                         if (MODE == 1) outp[i * out_stride + pos] = mi;
-                        else outp[pos * P.nq + P.col[i]] = mi;
+                        else outp[pos * P.nq + P.col[i]] = ld_nc(P.new2old + mi);
                     }
                 }
                 if (wr) {
                     if (MODE == 1) outp[d * out_stride + pos] = v;
-                    else outp[pos * P.nq + P.col[d]] = v;
+                    else outp[pos * P.nq + P.col[d]] = ld_nc(P.new2old + v);
                 }
             }
         }
@@ -643,7 +638,9 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
     if (MODE == 0 && lane == 0 && local) atomicAdd(ctr, local);
 }
 
-// Root candidates owned by this rank: cand bit of phi[0] set and (v / chunk) % world == rank.
+// Root candidates owned by this rank: cand bit of phi[0] set and (o / chunk) % world == rank
+// for the ORIGINAL id o (ownership is defined on the caller's ids; device ids are degree-
+// ordered and would put all hubs on one rank).  User roots arrive as original ids.
 __global__ void k_roots(const SearchParams P, unsigned long long n, const uint32_t *__restrict__ user,
                         unsigned long long nuser, uint32_t rank, uint32_t world, uint32_t chunk,
                         uint32_t *__restrict__ out, unsigned long long *__restrict__ ctr,
@@ -651,19 +648,21 @@ __global__ void k_roots(const SearchParams P, unsigned long long n, const uint32
     const unsigned long long total = user ? nuser : n;
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long v = user ? user[i] : i;
-        bool ok = v < n && (v / chunk) % world == rank;
+        const unsigned long long o = user ? user[i] : P.new2old[i];
+        bool ok = o < n && (o / chunk) % world == rank;
+        if (!ok) continue;
+        const uint32_t v = user ? P.old2new[o] : (uint32_t)i;
         uint32_t scratch = 0;
-        if (ok) ok = vlab[v] == P.lab[0] && cand_bit(P, 0, (uint32_t)v, scratch);
-        if (ok) out[atomicAdd(ctr, 1ull)] = (uint32_t)v;
+        ok = vlab[v] == P.lab[0] && cand_bit(P, 0, v, scratch);
+        if (ok) out[atomicAdd(ctr, 1ull)] = v;
     }
 }
 
 __global__ void k_write_single(const uint32_t *__restrict__ roots, unsigned long long n, uint32_t *__restrict__ out,
-                               unsigned long long cap) {
+                               unsigned long long cap, const uint32_t *__restrict__ new2old) {
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n && i < cap;
          i += (unsigned long long)gridDim.x * blockDim.x)
-        out[i] = roots[i];
+        out[i] = new2old[roots[i]];
 }
 
 __global__ void k_read_timer(unsigned long long *t) { *t = globaltimer(); }
@@ -810,9 +809,11 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.candoff[l] = p->order[l] * p->words;
         P.col[l] = p->order[l];
     }
-    P.hub_id = g->nhubs ? g->hub_id : nullptr;
+    P.nhubs = g->nhubs;
     P.hub_bits = g->hub_bits;
     P.hub_words = g->hub_words;
+    P.new2old = g->new2old;
+    P.old2new = g->old2new;
     if (!W.ctrl) GM_CK(cudaMalloc(&W.ctrl, sizeof(Ctrl)));
     GM_CK(cudaMemsetAsync(W.ctrl, 0, sizeof(Ctrl), st));
     P.ctrl = W.ctrl;
@@ -855,7 +856,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             uint32_t *dst = out;
             uint32_t *tmp = nullptr;
             if (mem == GM_MEM_HOST) { GM_CK(cudaMalloc(&tmp, sizeof(uint32_t) * std::max<uint64_t>(1, std::min<uint64_t>(cap, nroots)))); dst = tmp; }
-            k_write_single<<<grid_for(nroots, 256, W.sms), 256, 0, st>>>(frontier, nroots, dst, cap);
+            k_write_single<<<grid_for(nroots, 256, W.sms), 256, 0, st>>>(frontier, nroots, dst, cap, g->new2old);
             ++launches;
             if (tmp) {
                 GM_CK(cudaMemcpyAsync(out, tmp, sizeof(uint32_t) * std::min<uint64_t>(cap, nroots), cudaMemcpyDeviceToHost, st));
