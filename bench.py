@@ -41,6 +41,14 @@ CONFIGS = {
     "rmat22": dict(kind="rmat", scale=22, ef=16, labels=1, qsize=0, dense=[], sparse=[],
                    fixed=["triangle", "clique4", "cycle5"], limit_ms=5000.0, seed=3,
                    desc="R-MAT scale 22 unlabelled (4.2M vertices, ~64M edges): triangle / 4-clique / 5-cycle"),
+    "rmat24": dict(kind="rmat", scale=24, ef=8, labels=16, qsize=16, dense=[1000, 1001, 1002, 1003],
+                   sparse=[], limit_ms=2000.0, seed=4,
+                   desc="LiveJournal-shaped R-MAT scale 24 (16.8M vertices, ~265M adjacency entries, 16 labels), "
+                        "16-vertex dense queries"),
+    "rmat26": dict(kind="rmat", scale=26, ef=16, labels=16, qsize=[24, 24, 32, 32], dense=[1000, 1001, 1002, 1003],
+                   sparse=[], limit_ms=2000.0, seed=5,
+                   desc="Friendster-shaped R-MAT scale 26 (67M vertices, ~2.1B adjacency entries, 16 labels), "
+                        "24/32-vertex dense queries under a per-query time limit"),
 }
 
 
@@ -51,13 +59,15 @@ def env_int(k, d):
         return d
 
 
-def build_queries(cfg, off, nb, lab):
+def build_queries(cfg, adj, lab):
+    """The config's query set; adj = gminputs.HostAdjacency or gminputs.gpu.DeviceNeighbors."""
     import gminputs as gi
     qs = []
-    for s in cfg.get("dense", []):
-        qs.append(gi.random_query(off, nb, lab, cfg["qsize"], seed=s, dense=True, min_avg_degree=3.0))
+    sizes = cfg["qsize"] if isinstance(cfg["qsize"], list) else [cfg["qsize"]] * len(cfg.get("dense", []))
+    for s, k in zip(cfg.get("dense", []), sizes):
+        qs.append(gi.grow_query(adj, lab, k, seed=s, dense=True, min_avg_degree=3.0))
     for s in cfg.get("sparse", []):
-        qs.append(gi.random_walk_query(off, nb, lab, cfg["qsize"], seed=s))
+        qs.append(gi.walk_query(adj, lab, cfg["qsize"], seed=s))
     fx = cfg.get("fixed")
     if fx:
         for name in ([fx] if isinstance(fx, str) else fx):
@@ -164,8 +174,7 @@ def run_reference(args, cfg, world, rank):
     import gminputs as gi
     from oracle import OracleGraph
     n, s, d, lab = make_graph_host(cfg)
-    off, nb = gi.simple_adjacency(n, s, d)
-    qs = build_queries(cfg, off, nb, lab)
+    qs = build_queries(cfg, gi.HostAdjacency(*gi.simple_adjacency(n, s, d)), lab)
     og = OracleGraph(n, s, d, lab)
     budget_s = float(os.environ.get("GM_REF_STEP_S", "4.0"))
     rs = np.random.default_rng(0)
@@ -261,13 +270,21 @@ def main():
 
     # ---- inputs: graph generated on this GPU (replica per rank); queries from host adjacency
     n, s_dev, d_dev, lab_dev = make_graph_device(cfg)
-    s_h = s_dev.cpu().numpy().view(np.uint32)
-    d_h = d_dev.cpu().numpy().view(np.uint32)
     lab_h = lab_dev.cpu().numpy().view(np.uint32)
-    off, nb = gi.simple_adjacency(n, s_h, d_h)
-    qs = build_queries(cfg, off, nb, lab_h)
+    small = cfg["kind"] != "rmat" or cfg["scale"] <= 20
+    s_h = d_h = None
+    if small:                                    # host copy for query growth + the oracle baseline
+        s_h = s_dev.cpu().numpy().view(np.uint32)
+        d_h = d_dev.cpu().numpy().view(np.uint32)
+        adj = gi.HostAdjacency(*gi.simple_adjacency(n, s_h, d_h))
+    else:                                        # grow queries by scanning the device edge list
+        import gminputs.gpu as gg
+        adj = gg.DeviceNeighbors(n, s_dev, d_dev)
+    qs = build_queries(cfg, adj, lab_h)
+    del adj
     g = gm.gm_load_graph(n, s_dev, d_dev, lab_dev, cfg["labels"])
     del s_dev, d_dev
+    torch.cuda.empty_cache()
     ginfo = g.info()
     stream = torch.cuda.current_stream()
     run_kw = dict(tau=int(args.tau), rank=rank, world=world, steal=not args.no_steal, time_limit_ms=limit)
@@ -413,8 +430,12 @@ def main():
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:
-        n_, s_, d_, l_ = n, s_h, d_h, lab_h
-        line["cpu_baseline"] = cpu_baseline(cfg, qs, n_, s_, d_, l_)
+        if s_h is not None:
+            line["cpu_baseline"] = cpu_baseline(cfg, qs, n, s_h, d_h, lab_h)
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "embeddings/s", "cores": 1, "kind": "oracle",
+                                    "sample": "not run: building the oracle's host CSR for this graph size "
+                                              "exceeds the bench time budget"}
     if args.per_query:
         print(json.dumps(per_query), file=sys.stderr)
     print(json.dumps(line), flush=True)

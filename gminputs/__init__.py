@@ -185,16 +185,34 @@ class Query:
         return f"Query({self.name!r}, n={self.n}, m={len(self.edges)})"
 
 
-def random_query(offs, nbrs, labels, size: int, seed: int, max_restarts: int = 1000,
-                 dense: bool = False, min_avg_degree: float = 0.0) -> Query:
+class HostAdjacency:
+    """neighbors(v) of the simple graph, from host CSR arrays (simple_adjacency)."""
+
+    def __init__(self, offs, nbrs):
+        self.offs, self.nbrs = offs, nbrs
+        self.n = len(offs) - 1
+
+    def neighbors(self, v):
+        return self.nbrs[int(self.offs[v]):int(self.offs[v + 1])]
+
+
+def random_query(offs, nbrs, labels, size: int, seed: int, **kw) -> Query:
+    """grow_query over host CSR arrays."""
+    return grow_query(HostAdjacency(offs, nbrs), labels, size, seed, **kw)
+
+
+def grow_query(adj, labels, size: int, seed: int, max_restarts: int = 1000,
+               dense: bool = False, min_avg_degree: float = 0.0) -> Query:
     """§6.1 procedure: random seed vertex, repeatedly add a uniformly random vertex
     adjacent to the current set, keep ALL edges among chosen vertices (induced).
+    `adj` provides .n and .neighbors(v) (sorted, simple graph): HostAdjacency or the
+    device-scanning gminputs.gpu.DeviceNeighbors -- both give identical queries.
 
     dense=True draws the next vertex uniformly among the frontier vertices with the MOST
     neighbours in the chosen set (on sparse power-law graphs the plain procedure almost
     always returns trees; Appendix A's "dense" class needs d_avg >= 3).  Restarts until
     the query's average degree reaches min_avg_degree."""
-    n = len(offs) - 1
+    n = adj.n
     ctr = 0
     for _ in range(max_restarts):
         r = int(rng_u64(seed, STREAM_QUERY, ctr)); ctr += 1
@@ -204,7 +222,7 @@ def random_query(offs, nbrs, labels, size: int, seed: int, max_restarts: int = 1
         while len(chosen) < size:
             conn = {}
             for v in chosen:
-                for w in nbrs[int(offs[v]):int(offs[v + 1])]:
+                for w in adj.neighbors(v):
                     w = int(w)
                     if w not in cset:
                         conn[w] = conn.get(w, 0) + 1
@@ -221,38 +239,42 @@ def random_query(offs, nbrs, labels, size: int, seed: int, max_restarts: int = 1
             cset.add(w)
         if len(chosen) == size:
             idx = {v: i for i, v in enumerate(chosen)}
-            m = sum(1 for v in chosen for w in nbrs[int(offs[v]):int(offs[v + 1])] if int(w) in idx) // 2
-            if 2.0 * m / size < min_avg_degree:
-                continue
-            idx = {v: i for i, v in enumerate(chosen)}
             edges = []
             for v in chosen:
-                for w in nbrs[offs[v]:offs[v + 1]]:
+                for w in adj.neighbors(v):
                     w = int(w)
                     if w in idx and idx[v] < idx[w]:
                         edges.append((idx[v], idx[w]))
+            if 2.0 * len(edges) / size < min_avg_degree:
+                continue
             return Query(size, edges, [int(labels[v]) for v in chosen], name=f"rq{size}_s{seed}")
     raise RuntimeError("random_query: could not grow a connected query (isolated region)")
 
 
-def random_walk_query(offs, nbrs, labels, size: int, seed: int, max_steps: int = 100000) -> Query:
+def random_walk_query(offs, nbrs, labels, size: int, seed: int, **kw) -> Query:
+    """walk_query over host CSR arrays."""
+    return walk_query(HostAdjacency(offs, nbrs), labels, size, seed, **kw)
+
+
+def walk_query(adj, labels, size: int, seed: int, max_steps: int = 100000) -> Query:
     """Sparse variant: a random walk from a random vertex until `size` distinct vertices
     are visited; only the traversed edges are kept (a spanning tree plus revisits)."""
-    n = len(offs) - 1
+    n = adj.n
     ctr = 0
     for _ in range(1000):
         r = int(rng_u64(seed, STREAM_QUERY, ctr)); ctr += 1
         cur = r % n
-        if int(offs[cur + 1]) == int(offs[cur]):
+        if len(adj.neighbors(cur)) == 0:
             continue
         idx = {cur: 0}
         order = [cur]
         edges = set()
         steps = 0
         while len(order) < size and steps < max_steps:
-            deg = int(offs[cur + 1] - offs[cur])
+            nb = adj.neighbors(cur)
+            deg = len(nb)
             r = int(rng_u64(seed, STREAM_QUERY, ctr)); ctr += 1
-            nxt = int(nbrs[int(offs[cur]) + r % deg])
+            nxt = int(nb[r % deg])
             if nxt not in idx:
                 idx[nxt] = len(order)
                 order.append(nxt)

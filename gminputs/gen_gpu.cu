@@ -71,6 +71,19 @@ __global__ void k_incident(uint64_t m, const uint32_t *src, const uint32_t *dst,
     }
 }
 
+// The other endpoints of all edges incident to vertex v (duplicates / self loops included;
+// the caller dedups) -- neighbour lists of a device-resident edge list, for query growth.
+__global__ void k_neighbors(uint64_t m, const uint32_t *src, const uint32_t *dst, uint32_t v, uint32_t *out,
+                            unsigned long long *cnt, uint64_t cap) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = src[e], b = dst[e];
+        if (a == v || b == v) {
+            const unsigned long long k = atomicAdd(cnt, 1ull);
+            if (k < cap) out[k] = a == v ? b : a;
+        }
+    }
+}
+
 static int grid(uint64_t work) {
     uint64_t g = (work + 255) / 256;
     if (g > 148ull * 64) g = 148ull * 64;
@@ -90,6 +103,12 @@ GEN_API int gen_er(uint64_t n, uint64_t m, uint64_t seed, uint32_t *src, uint32_
 
 GEN_API int gen_labels(uint64_t n, uint32_t S, uint64_t seed, uint32_t *lab, void *stream) {
     k_labels<<<grid(n), 256, 0, (cudaStream_t)stream>>>(n, S, stream_key(seed, 3), lab);
+    return (int)cudaGetLastError();
+}
+
+GEN_API int gen_neighbors(uint64_t m, const uint32_t *src, const uint32_t *dst, uint32_t v, uint32_t *out,
+                          unsigned long long *cnt, uint64_t cap, void *stream) {
+    k_neighbors<<<grid(m), 256, 0, (cudaStream_t)stream>>>(m, src, dst, v, out, cnt, cap);
     return (int)cudaGetLastError();
 }
 

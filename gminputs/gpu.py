@@ -32,6 +32,7 @@ def _load():
         L.gen_er.argtypes = [u64, u64, u64, vp, vp, vp]
         L.gen_labels.argtypes = [u64, ctypes.c_uint32, u64, vp, vp]
         L.gen_incident.argtypes = [u64, vp, vp, vp, vp, vp, vp, u64, vp]
+        L.gen_neighbors.argtypes = [u64, vp, vp, ctypes.c_uint32, vp, vp, u64, vp]
         _lib = L
     return _lib
 
@@ -71,13 +72,36 @@ def uniform_labels(n, num_labels, seed, device="cuda"):
 
 
 class DeviceNeighbors:
-    """neighbors(v) for a device-resident edge list (scan of all edges per call)."""
+    """neighbors(v) of the simple graph on a device-resident edge list: one scan of all
+    edges per new vertex (cached), so query growth on scale-24/26 graphs needs no host CSR.
+    Gives the same sorted, deduplicated lists as gminputs.HostAdjacency."""
 
     def __init__(self, n, src, dst):
         import torch
         self.n, self.src, self.dst = n, src, dst
         self.bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device=src.device)
         self.cnt = torch.zeros(1, dtype=torch.int64, device=src.device)
+        self.cache = {}
+
+    def neighbors(self, v):
+        v = int(v)
+        if v in self.cache:
+            return self.cache[v]
+        import torch
+        cap = 1 << 16
+        while True:
+            self.cnt.zero_()
+            out = torch.empty(cap, dtype=torch.int32, device=self.src.device)
+            assert _load().gen_neighbors(self.src.numel(), self.src.data_ptr(), self.dst.data_ptr(), v,
+                                         out.data_ptr(), self.cnt.data_ptr(), cap, _stream()) == 0
+            k = int(self.cnt.item())
+            if k <= cap:
+                break
+            cap = 1 << int(np.ceil(np.log2(k)))
+        nb = out[:k].cpu().numpy().view(np.uint32)
+        nb = np.unique(nb[nb != v])
+        self.cache[v] = nb
+        return nb
 
     def of_set(self, vs):
         """{v: sorted neighbour array} for every v in vs (one edge scan)."""

@@ -336,7 +336,7 @@ def test_config2_sampled_roots(gm):
     cfg = bench.CONFIGS["rmat18"]
     n, s, d, lab = bench.make_graph_host(cfg)
     off, nb = gi.simple_adjacency(n, s, d)
-    queries = bench.build_queries(cfg, off, nb, lab)          # the bench's query set
+    queries = bench.build_queries(cfg, gi.HostAdjacency(off, nb), lab)          # the bench's query set
     g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
     og = OracleGraph(n, s, d, lab)
     rs = np.random.default_rng(1)

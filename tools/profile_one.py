@@ -19,7 +19,7 @@ cfg = bench.CONFIGS[cfgname]
 n, s, d, lab = bench.make_graph_device(cfg)
 sh, dh, lh = (x.cpu().numpy().view(np.uint32) for x in (s, d, lab))
 off, nb = gi.simple_adjacency(n, sh, dh)
-qs = bench.build_queries(cfg, off, nb, lh)
+qs = bench.build_queries(cfg, gi.HostAdjacency(off, nb), lh)
 g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
 q = qs[qi]
 p = gm.gm_plan_query(g, q)
