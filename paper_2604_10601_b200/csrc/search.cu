@@ -49,6 +49,7 @@ struct Ctrl {
     alignas(128) unsigned long long q_head;   // ring positions (monotone, 64-bit: never wrap)
     alignas(128) unsigned long long q_tail;
     alignas(128) int abort;
+    unsigned long long t0;                    // globaltimer at the first warp's start
     alignas(128) unsigned long long out_ctr;
     alignas(128) unsigned long long count;
     unsigned long long tasks;
@@ -65,6 +66,7 @@ struct SearchParams {
     uint32_t lab[kMaxQ];        // L(phi[l])
     uint32_t bw[kMaxQ];         // backward positions of phi[l]
     uint32_t candoff[kMaxQ];    // word offset of phi[l]'s candidate bitmap (phi[l] * words)
+    uint32_t cand_needed;       // bit l: the filter of phi[l] is not implied by its backward edges
     uint32_t col[kMaxQ];        // output column of position l (= phi[l])
     const uint32_t *pool;       // level-major, pool_size items of depth d0
     unsigned long long pool_size;
@@ -86,7 +88,7 @@ struct SearchParams {
     uint32_t last_adj;          // positions adjacent to phi[last_b] in Q
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
-    unsigned long long deadline_ns;  // 0 = no limit
+    unsigned long long limit_ns;     // time limit of this launch (0 = none)
 };
 
 // ------------------------------------------------------------------ device helpers
@@ -187,7 +189,7 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 template <int D>
 __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
                                         bool has, uint32_t lane, uint32_t &words) {
-    bool ok = has && cand_bit(P, l, v, words);
+    bool ok = has && (!((P.cand_needed >> l) & 1u) || cand_bit(P, l, v, words));
     const uint32_t cs = has ? S.cs[l][src] : 0u;
     const uint32_t chk = P.bw[l] & ~(1u << cs);
     const uint32_t lab = P.lab[l];
@@ -321,6 +323,8 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
     uint32_t tick = 0;
     bool stop = false;
     bool registered = false;   // this idle warp has posted a steal request
+    // time limit relative to this launch: the first warp to start stamps t0
+    if (P.limit_ns && lane == 0) atomicCAS(&C->t0, 0ull, globaltimer());
 
     while (!stop) {
         // ------------------------------------------------ acquire a unit of work
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
             if (((++tick) & 31u) == 0) {
                 int ab = 0, claim = 0;
                 if (lane == 0) {
-                    if (P.deadline_ns && globaltimer() > P.deadline_ns) atomicExch(&C->abort, 1);
+                    if (P.limit_ns && globaltimer() > VC->t0 + P.limit_ns) atomicExch(&C->abort, 1);
                     ab = VC->abort;
                     // work stealing (§4.3): serve one posted request by splitting our stack
                     if (P.steal && VC->requests > 0) {
@@ -765,6 +769,13 @@ extern "C" void gm_default_opts(gm_run_opts *o) {
     o->pool_bytes_max = 1ull << 30;
 }
 
+// Query-vertex bitmask (by query vertex id) of phi[0..l-1].
+static uint32_t backward_vertices(const gm_plan *p, uint32_t l) {
+    uint32_t m = 0;
+    for (uint32_t i = 0; i < l; ++i) m |= 1u << p->order[i];
+    return m;
+}
+
 static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumerate, uint32_t *out, uint64_t cap,
                       int mem, uint64_t *count_out, int count_mem, gm_run_stats *stats, cudaStream_t st) {
     set_error("");
@@ -807,6 +818,12 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.lab[l] = p->qlab[p->order[l]] < g->S ? p->qlab[p->order[l]] : 0xfffffffeu;
         P.bw[l] = p->bw[l];
         P.candoff[l] = p->order[l] * p->words;
+        // LDF/NLF count neighbours of u by label; if ALL of u's query neighbours precede it in
+        // phi, a candidate adjacent to their (distinct, label-matching) images already meets
+        // both bounds, so the bitmap test is implied and skipped (level 0 always tests).
+        // With GM_FILTER_NONE the bitmap is the label test, implied by the label-partitioned slice.
+        if (l == 0 || (p->filter != GM_FILTER_NONE && (p->qadj[p->order[l]] & ~backward_vertices(p, l)) != 0))
+            P.cand_needed |= 1u << l;
         P.col[l] = p->order[l];
     }
     P.nhubs = g->nhubs;
@@ -932,18 +949,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.steal = o.steal ? 1 : 0;
         P.q_items = W.q_items; P.q_seq = W.q_seq; P.q_cap = o.steal ? W.q_cap : 1;
         if (enumerate) { P.out = out_dev(); P.out_cap = cap; }
-        unsigned long long deadline = 0;
-        if (o.time_limit_ms > 0) {
-            // deadline on the device's %globaltimer clock (ns), read by a 1-thread kernel
-            unsigned long long *d_t = &W.ctrl->tasks;   // scratch (zeroed below)
-            k_read_timer<<<1, 1, 0, st>>>(d_t);
-            GM_CK(cudaMemcpyAsync(&deadline, d_t, sizeof(deadline), cudaMemcpyDeviceToHost, st));
-            GM_CK(cudaStreamSynchronize(st));
-            deadline += (unsigned long long)(o.time_limit_ms * 1e6);
-            GM_CK(cudaMemsetAsync(d_t, 0, sizeof(unsigned long long), st));
-            ++launches;
-        }
-        P.deadline_ns = deadline;
+        // the time limit covers the DFS launch (the BFS init phase is short and bounded by tau)
+        P.limit_ns = o.time_limit_ms > 0 ? (unsigned long long)(o.time_limit_ms * 1e6) : 0ull;
         {   // last-level set counting applies when phi[last] has exactly one backward neighbour
             const uint32_t last = p->nq - 1, bwl = p->bw[last];
             if (!enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && last >= 1 && __builtin_popcount(bwl) == 1) {

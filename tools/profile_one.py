@@ -28,7 +28,7 @@ cands = np.flatnonzero(p.candidates(u0))
 roots = np.random.default_rng(0).permutation(cands)[:nroots].astype(np.uint32) if nroots > 0 else None
 for it in range(2):
     t = time.time()
-    c, st = gm.gm_count(p, roots=roots, tau=tau)
+    c, st = gm.gm_count(p, roots=roots, tau=tau, time_limit_ms=float(os.environ.get("GM_LIMIT_MS", "0")))
     print(q.name, len(q.edges), c, f"wall {time.time() - t:.3f}s",
           {k: st[k] for k in ("dfs_ms", "total_ms", "tasks", "words", "pool_size", "pool_depth", "donations",
                               "grid", "block")}, flush=True)
