@@ -67,6 +67,8 @@ struct SearchParams {
     uint32_t bw[kMaxQ];         // backward positions of phi[l]
     uint32_t candoff[kMaxQ];    // word offset of phi[l]'s candidate bitmap (phi[l] * words)
     uint32_t cand_needed;       // bit l: the filter of phi[l] is not implied by its backward edges
+    uint32_t same_lab[kMaxQ];   // bit i of same_lab[l]: i < l and L(phi[i]) == L(phi[l])
+    uint32_t walk_low[kMaxQ];   // lowest level process() must visit at level l (l if none)
     uint32_t col[kMaxQ];        // output column of position l (= phi[l])
     const uint32_t *pool;       // level-major, pool_size items of depth d0
     unsigned long long pool_size;
@@ -86,6 +88,7 @@ struct SearchParams {
     uint32_t last_b;            // position of phi[last]'s single backward neighbour
     uint32_t last_same;         // positions i < last, i != last_b, with L(phi[i]) == L(phi[last])
     uint32_t last_adj;          // positions adjacent to phi[last_b] in Q
+    uint32_t last_low;          // deepest level count_last must visit
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
@@ -189,15 +192,26 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 template <int D>
 __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
                                         bool has, uint32_t lane, uint32_t &words) {
-    bool ok = has && (!((P.cand_needed >> l) & 1u) || cand_bit(P, l, v, words));
+    // The candidate-bitmap word is loaded now but tested last, so its L2 round trip overlaps
+    // the chain walk and the adjacency probes instead of gating them.
+    uint32_t cword = 0xffffffffu;
+    if (has && ((P.cand_needed >> l) & 1u)) {
+        cword = ld_nc(P.cand + P.candoff[l] + (v >> 5));
+        ++words;
+    }
+    bool ok = has;
     const uint32_t cs = has ? S.cs[l][src] : 0u;
     const uint32_t chk = P.bw[l] & ~(1u << cs);
     const uint32_t lab = P.lab[l];
+    // Only levels holding a backward neighbour (adjacency check) or a vertex of v's label
+    // (v can only collide with a same-label image) need visiting; the walk stops at the
+    // deepest such level, uniformly across lanes (P.walk_low[l]).
+    const uint32_t eq = P.same_lab[l];
     uint32_t p = src;
     int k = 0;
-    for (int i = l - 1; i >= 0; --i) {              // injectivity + collect the checks
+    for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
         const uint32_t w = S.v[i][p];
-        ok = ok && (w != v);
+        if ((eq >> i) & 1u) ok = ok && (w != v);
         if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
         p = S.pid[i][p];
     }
@@ -254,7 +268,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         if (need1) { r1 = n1 == 1 && ld_nc(P.nbr + b1) == v; words += n1; }
         ok = ok && r0 && r1;
     }
-    return ok;
+    return ok && ((cword >> (v & 31)) & 1u);
 }
 
 // Last-level set counting (count mode): when phi[last] has ONE
@@ -266,34 +280,30 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 // (adj_b), else one binary search decides.  Cost O(|M|) instead of O(|slice|) tasks.
 // (l, v, src) is the task that just completed M at level l = last - 1.
 template <int D>
-__device__ __forceinline__ uint32_t count_last(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t v,
-                                               uint32_t src, uint32_t &words) {
+__device__ __forceinline__ uint32_t count_last(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v,
+                                               uint32_t src, uint32_t lane, uint32_t &words) {
     const int b = (int)P.last_b;
     const uint32_t lab = P.lab[l + 1];
-    uint32_t mb = v;                      // M[b]
-    if (b != l) {
-        uint32_t p = src;
-        for (int i = l - 1; i > b; --i) p = S.pid[i][p];
-        mb = S.v[b][p];
+    const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
+    // one walk from level l-1 down to the deepest level needed: fetch M[b], and park the
+    // same-label images that need an adjacency test in the lane's scratch column
+    uint32_t mb = v;                      // M[b] (b == l: the task itself)
+    int k = 0;
+    uint32_t p = src;
+    for (int i = l - 1; i >= (int)P.last_low; --i) {
+        const uint32_t w = S.v[i][p];
+        if (i == b) mb = w;
+        if (((same >> i) & 1u) && !((P.last_adj >> i) & 1u)) { S.chk[k][lane] = w; ++k; }
+        p = S.pid[i][p];
     }
     const uint32_t row = mb * P.S + lab;
     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
     words += 2;
-    uint32_t cnt = hi - lo;
-    uint32_t same = P.last_same;          // positions i < last, i != b, with L(phi[i]) == lab
-    if (same) {
-        if ((same >> l) & 1u) {
-            if (((P.last_adj >> l) & 1u) || has_edge(P, mb, lab, v, words)) --cnt;
-        }
-        uint32_t p = src;
-        for (int i = l - 1; i >= 0 && (same & ((1u << (i + 1)) - 1)); --i) {
-            if ((same >> i) & 1u) {
-                const uint32_t w = S.v[i][p];
-                if (((P.last_adj >> i) & 1u) || has_edge(P, mb, lab, w, words)) --cnt;
-            }
-            p = S.pid[i][p];
-        }
-    }
+    // mapped vertices adjacent to phi[b] in Q lie in the slice for sure (same label)
+    uint32_t cnt = hi - lo - (uint32_t)__popc(same & P.last_adj & ((2u << l) - 1));
+    if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lab, v, words)) --cnt;
+    for (int c = 0; c < k; ++c)
+        if (has_edge(P, mb, lab, S.chk[c][lane], words)) --cnt;
     return cnt;
 }
 
@@ -540,7 +550,7 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
             if (!ENUM && P.bulk_last && l == last - 1) {
                 // last-level set counting: the extensions of this partial match are exactly the
                 // label-L(phi[last]) neighbours of its backward neighbour minus the mapped ones
-                if (F) my_count += count_last<D>(P, S, l, v, src, wacc);
+                if (F) my_count += count_last<D>(P, S, l, v, src, lane, wacc);
                 __syncwarp();
                 continue;
             }
@@ -824,6 +834,10 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         // With GM_FILTER_NONE the bitmap is the label test, implied by the label-partitioned slice.
         if (l == 0 || (p->filter != GM_FILTER_NONE && (p->qadj[p->order[l]] & ~backward_vertices(p, l)) != 0))
             P.cand_needed |= 1u << l;
+        for (uint32_t i = 0; i < l; ++i)
+            if (p->qlab[p->order[i]] == p->qlab[p->order[l]]) P.same_lab[l] |= 1u << i;
+        const uint32_t need = P.same_lab[l] | p->bw[l];
+        P.walk_low[l] = need ? (uint32_t)__builtin_ctz(need) : l;
         P.col[l] = p->order[l];
     }
     P.nhubs = g->nhubs;
@@ -961,6 +975,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                     if (i != b && p->qlab[p->order[i]] == p->qlab[p->order[last]]) P.last_same |= 1u << i;
                     if ((p->qadj[p->order[b]] >> p->order[i]) & 1u) P.last_adj |= 1u << i;
                 }
+                const uint32_t l = last - 1;   // the level count_last runs at
+                const uint32_t need = (b < l ? 1u << b : 0u) | (P.last_same & ~P.last_adj & ((1u << l) - 1));
+                P.last_low = need ? (uint32_t)__builtin_ctz(need) : l;
             }
         }
         GM_CK(cudaEventRecord(d0e, st));
