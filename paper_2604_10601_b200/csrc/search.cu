@@ -88,7 +88,8 @@ struct SearchParams {
     uint32_t last_b;            // position of phi[last]'s single backward neighbour
     uint32_t last_same;         // positions i < last, i != last_b, with L(phi[i]) == L(phi[last])
     uint32_t last_adj;          // positions adjacent to phi[last_b] in Q
-    uint32_t last_low;          // deepest level count_last must visit
+    uint32_t last_low;          // deepest level prep_last must visit
+    uint32_t last_k;            // popc(last_same & ~last_adj & below last-1): parked images per parent
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
@@ -148,6 +149,8 @@ struct WarpStack {
     uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
     uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
     uint32_t chk[D][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
+    uint32_t lastw[D][32];// set counting: per parent lane at level last-2, the same-label images to test
+    uint32_t lastmb[32];  //               and the image of phi[last]'s backward neighbour (if < last-1)
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
 };
@@ -192,8 +195,8 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 template <int D>
 __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
                                         bool has, uint32_t lane, uint32_t &words) {
-    // The candidate-bitmap word is loaded now but tested last, so its L2 round trip overlaps
-    // the chain walk and the adjacency probes instead of gating them.
+    // The candidate-bitmap word is loaded first and tested after the chain walk, so its L2
+    // round trip overlaps the walk; it still gates the (costlier) adjacency probes.
     uint32_t cword = 0xffffffffu;
     if (has && ((P.cand_needed >> l) & 1u)) {
         cword = ld_nc(P.cand + P.candoff[l] + (v >> 5));
@@ -215,6 +218,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
         p = S.pid[i][p];
     }
+    ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
     const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
     // Two checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
     // independent, so each lane keeps two dependent-load chains in flight (ncu: the kernel
@@ -268,7 +272,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         if (need1) { r1 = n1 == 1 && ld_nc(P.nbr + b1) == v; words += n1; }
         ok = ok && r0 && r1;
     }
-    return ok && ((cword >> (v & 31)) & 1u);
+    return ok;
 }
 
 // Last-level set counting (count mode): when phi[last] has ONE
@@ -279,31 +283,41 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 // L(phi[i]) = L(phi[last]) (bitmask same_lab); it surely does if phi[i] ~ phi[b] in Q
 // (adj_b), else one binary search decides.  Cost O(|M|) instead of O(|slice|) tasks.
 // (l, v, src) is the task that just completed M at level l = last - 1.
+//
+// The part that depends only on the parent (levels < l) is computed once per parent lane when
+// level l = last-1 is entered (prep_last), not once per task: M[b] when b < l, and the
+// same-label images not adjacent to phi[b] in Q (those need an adjacency test).
 template <int D>
-__device__ __forceinline__ uint32_t count_last(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v,
-                                               uint32_t src, uint32_t lane, uint32_t &words) {
+__device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane) {
+    if (!valid) return;
     const int b = (int)P.last_b;
-    const uint32_t lab = P.lab[l + 1];
-    const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
-    // one walk from level l-1 down to the deepest level needed: fetch M[b], and park the
-    // same-label images that need an adjacency test in the lane's scratch column
-    uint32_t mb = v;                      // M[b] (b == l: the task itself)
+    const uint32_t test = P.last_same & ~P.last_adj;
+    uint32_t mb = 0;
     int k = 0;
-    uint32_t p = src;
+    uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.last_low; --i) {
         const uint32_t w = S.v[i][p];
         if (i == b) mb = w;
-        if (((same >> i) & 1u) && !((P.last_adj >> i) & 1u)) { S.chk[k][lane] = w; ++k; }
+        if ((test >> i) & 1u) { S.lastw[k][lane] = w; ++k; }
         p = S.pid[i][p];
     }
+    S.lastmb[lane] = mb;
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t count_last(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t v,
+                                               uint32_t src, uint32_t &words) {
+    const uint32_t lab = P.lab[l + 1];
+    const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
+    const uint32_t mb = (int)P.last_b == l ? v : S.lastmb[src];   // M[b]
     const uint32_t row = mb * P.S + lab;
     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
     words += 2;
     // mapped vertices adjacent to phi[b] in Q lie in the slice for sure (same label)
     uint32_t cnt = hi - lo - (uint32_t)__popc(same & P.last_adj & ((2u << l) - 1));
     if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lab, v, words)) --cnt;
-    for (int c = 0; c < k; ++c)
-        if (has_edge(P, mb, lab, S.chk[c][lane], words)) --cnt;
+    for (uint32_t c = 0; c < P.last_k; ++c)
+        if (has_edge(P, mb, lab, S.lastw[c][src], words)) --cnt;
     return cnt;
 }
 
@@ -381,6 +395,7 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
+                if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, d0, valid, lane);
                 base = d0; l = d0;
                 got = true;
                 break;
@@ -399,6 +414,7 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
                     __threadfence();
                     ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                 }
+                if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, depth, lane == 0, lane);
                 base = (int)depth; l = (int)depth;
                 got = true;
                 break;
@@ -550,7 +566,7 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
             if (!ENUM && P.bulk_last && l == last - 1) {
                 // last-level set counting: the extensions of this partial match are exactly the
                 // label-L(phi[last]) neighbours of its backward neighbour minus the mapped ones
-                if (F) my_count += count_last<D>(P, S, l, v, src, lane, wacc);
+                if (F) my_count += count_last<D>(P, S, l, v, src, wacc);
                 __syncwarp();
                 continue;
             }
@@ -560,6 +576,7 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
             if (!fm) continue;
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
             generate<D>(P, S, l + 1, F, lane, wacc);
+            if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, l + 1, F, lane);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
             __syncwarp();
             ++l;
@@ -978,6 +995,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 const uint32_t l = last - 1;   // the level count_last runs at
                 const uint32_t need = (b < l ? 1u << b : 0u) | (P.last_same & ~P.last_adj & ((1u << l) - 1));
                 P.last_low = need ? (uint32_t)__builtin_ctz(need) : l;
+                P.last_k = (uint32_t)__builtin_popcount(P.last_same & ~P.last_adj & ((1u << l) - 1));
             }
         }
         GM_CK(cudaEventRecord(d0e, st));
