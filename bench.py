@@ -260,10 +260,15 @@ def main():
     import torch
     import torch.distributed as dist
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = local_rank % torch.cuda.device_count()   # one rank per GPU (ranks share a GPU only when
+    torch.cuda.set_device(gpu)                     # testing the multi-rank path on a 1-GPU box)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("GM_DIST_BACKEND", "nccl")   # gloo: several ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import gminputs as gi
     import paper_2604_10601_b200 as gm
     from paper_2604_10601_b200 import partition
@@ -312,7 +317,7 @@ def main():
         step(False)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     clocks.start()
     step_ms, dfs_ms, dfs_launches, words, kernel_launches = [], [], 0, 0, 0
     total_emb, q_ms, timeouts, tasks = 0, [], 0, 0
