@@ -141,6 +141,8 @@ typedef struct {
     uint32_t backward[GM_MAX_QUERY];    /* bit i of backward[l]: phi[i] is a backward
                                            neighbour of phi[l] (N_+^phi, Table 1) */
     uint64_t cand_count[GM_MAX_QUERY];  /* |C(u)| after filtering, by query vertex id */
+    uint64_t automorphisms;             /* |Aut(Q)| (label-preserving), 0 if not enumerated */
+    uint32_t sb_conditions;             /* number of symmetry-breaking conditions M[a] < M[b] */
 } gm_plan_info_t;
 
 GM_API int gm_plan_info(const gm_plan *p, gm_plan_info_t *info);
@@ -160,6 +162,8 @@ GM_API void gm_free_plan(gm_plan *p);
 #define GM_FLAG_NO_SET_COUNT 1u  /* gm_count: validate every last-level candidate as its own task
                                     (Alg. 2 as written) instead of set-counting the last level
                                     when phi[last] has a single backward neighbour */
+#define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
+                                    Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)| */
 
 typedef struct {
     uint64_t tau;            /* initial task-pool threshold (§4.3); 0 = 1e6 */
@@ -197,6 +201,7 @@ typedef struct {
     uint64_t words;           /* 4-byte words the DFS kernel read from the CSR and the candidate
                                  bitmaps: candidate reads + row-offset pairs + binary-search
                                  probes + bitmap words (algorithmic bytes = 4 * words) */
+    uint64_t automorphisms;   /* |Aut(Q)| the count was scaled by (1: no symmetry breaking) */
 } gm_run_stats;
 
 /*

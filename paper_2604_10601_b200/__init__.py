@@ -112,7 +112,8 @@ class Plan:
         L.check(L.lib().gm_plan_info(self._h, ctypes.byref(inf)))
         nq = inf.nq
         return {"nq": nq, "order": list(inf.order[:nq]), "backward": list(inf.backward[:nq]),
-                "cand_count": list(inf.cand_count[:nq])}
+                "cand_count": list(inf.cand_count[:nq]), "automorphisms": inf.automorphisms,
+                "sb_conditions": inf.sb_conditions}
 
     def candidates(self, u) -> np.ndarray:
         """Boolean mask over data vertices: passed the filter for query vertex u."""
@@ -176,7 +177,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
-          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True):
+          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -200,6 +201,8 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.pool_bytes_max = int(pool_bytes_max)
     if not set_count:
         o.flags |= L.GM_FLAG_NO_SET_COUNT
+    if not symmetry:
+        o.flags |= L.GM_FLAG_NO_SYMMETRY
     return o, keep
 
 

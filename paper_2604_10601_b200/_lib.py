@@ -19,6 +19,7 @@ GM_OK, GM_ERR_ARG, GM_ERR_CUDA, GM_ERR_NOMEM, GM_ERR_LIMIT, GM_TIMEOUT = 0, 1, 2
 GM_MEM_HOST, GM_MEM_DEVICE = 0, 1
 GM_MAX_QUERY = 32
 GM_FLAG_NO_SET_COUNT = 1
+GM_FLAG_NO_SYMMETRY = 2
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 
 # every symbol include/gmatch.h declares (checked by tests/test_abi.py)
@@ -37,7 +38,8 @@ class GraphInfo(ctypes.Structure):
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [("nq", ctypes.c_uint32), ("order", ctypes.c_uint32 * GM_MAX_QUERY),
-                ("backward", ctypes.c_uint32 * GM_MAX_QUERY), ("cand_count", ctypes.c_uint64 * GM_MAX_QUERY)]
+                ("backward", ctypes.c_uint32 * GM_MAX_QUERY), ("cand_count", ctypes.c_uint64 * GM_MAX_QUERY),
+                ("automorphisms", ctypes.c_uint64), ("sb_conditions", ctypes.c_uint32)]
 
 
 class RunOpts(ctypes.Structure):
@@ -55,7 +57,7 @@ class RunStats(ctypes.Structure):
                 ("donations", ctypes.c_uint64), ("tasks", ctypes.c_uint64), ("rounds", ctypes.c_uint64),
                 ("dfs_ms", ctypes.c_float), ("total_ms", ctypes.c_float), ("dfs_launches", ctypes.c_uint32),
                 ("kernel_launches", ctypes.c_uint32), ("grid", ctypes.c_uint32), ("block", ctypes.c_uint32),
-                ("words", ctypes.c_uint64)]
+                ("words", ctypes.c_uint64), ("automorphisms", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

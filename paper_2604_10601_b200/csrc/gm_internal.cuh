@@ -78,4 +78,10 @@ struct gm_plan {
     uint32_t filter = 0;
     uint32_t words = 0;             // ceil(n/32)
     uint32_t *cand = nullptr;       // nq * words bitmaps, by query vertex id
+    // symmetry breaking (plan.cu): |Aut(Q)| (label-preserving) and, per position l, the
+    // positions i < l with a condition M[phi[i]] < M[phi[l]] (sb_gt) or > (sb_lt)
+    uint64_t aut = 1;
+    bool sb_ok = false;             // conditions computed (|Aut| small enough to enumerate)
+    uint32_t sb_gt[gm::kMaxQ];      // v = M[phi[l]] must be greater than M[phi[i]]
+    uint32_t sb_lt[gm::kMaxQ];      // v must be smaller than M[phi[i]]
 };

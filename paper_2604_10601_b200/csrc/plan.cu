@@ -121,6 +121,74 @@ static void ri_order(const gm_plan *p, uint32_t *order) {
     }
 }
 
+// ---- symmetry breaking (Appendix A: "we use the same matching order and
+// symmetry breaking strategy in gMatch and T-DFS").  Aut(Q) = label- and edge-preserving
+// permutations of V(Q), enumerated by backtracking (given up above kMaxAut).  Conditions
+// are Grochow-Kellis: while the group is non-trivial, take the vertex v with the largest
+// orbit (earliest in phi on ties), require M[v] < M[w] for every other w of its orbit, and
+// continue with v's stabilizer.  Exactly one embedding of every Aut(Q)-orbit satisfies
+// them (the orbit of an embedding under Aut(Q) has |Aut(Q)| members, injectivity makes the
+// action free), so count = |Aut(Q)| * (embeddings satisfying the conditions).
+static constexpr size_t kMaxAut = 200000;
+
+static bool aut_search(const gm_plan *p, uint32_t pos, uint8_t *img, uint32_t used,
+                       std::vector<std::vector<uint8_t>> &auts) {
+    const uint32_t nq = p->nq;
+    if (pos == nq) {
+        auts.emplace_back(img, img + nq);
+        return auts.size() <= kMaxAut;
+    }
+    for (uint32_t w = 0; w < nq; ++w) {
+        if ((used >> w) & 1u) continue;
+        if (p->qlab[w] != p->qlab[pos] || p->qdeg[w] != p->qdeg[pos]) continue;
+        bool ok = true;
+        for (uint32_t x = 0; x < pos && ok; ++x)
+            ok = ((p->qadj[pos] >> x) & 1u) == ((p->qadj[w] >> img[x]) & 1u);
+        if (!ok) continue;
+        img[pos] = (uint8_t)w;
+        if (!aut_search(p, pos + 1, img, used | (1u << w), auts)) return false;
+    }
+    return true;
+}
+
+static void symmetry_conditions(gm_plan *p) {
+    const uint32_t nq = p->nq;
+    memset(p->sb_gt, 0, sizeof(p->sb_gt));
+    memset(p->sb_lt, 0, sizeof(p->sb_lt));
+    p->aut = 1;
+    p->sb_ok = false;
+    std::vector<std::vector<uint8_t>> auts;
+    uint8_t img[kMaxQ];
+    if (!aut_search(p, 0, img, 0u, auts)) return;     // group too large to enumerate: no SB
+    p->aut = auts.size();
+    std::vector<size_t> S(auts.size());
+    for (size_t i = 0; i < S.size(); ++i) S[i] = i;
+    while (S.size() > 1) {
+        int best = -1;
+        uint32_t best_orbit = 0, best_size = 0;
+        for (uint32_t l = 0; l < nq; ++l) {                // scan in phi order: earliest wins ties
+            const uint32_t v = p->order[l];
+            uint32_t orbit = 0;
+            for (size_t a : S) orbit |= 1u << auts[a][v];
+            const uint32_t sz = (uint32_t)__builtin_popcount(orbit);
+            if (sz > best_size) { best = (int)v; best_orbit = orbit; best_size = sz; }
+        }
+        if (best_size <= 1) break;
+        const uint32_t v = (uint32_t)best;
+        for (uint32_t w = 0; w < nq; ++w) {
+            if (w == v || !((best_orbit >> w) & 1u)) continue;
+            // condition M[v] < M[w], checked when the later of the two is mapped
+            const uint32_t lv = p->pos[v], lw = p->pos[w];
+            if (lv < lw) p->sb_gt[lw] |= 1u << lv;
+            else p->sb_lt[lv] |= 1u << lw;
+        }
+        std::vector<size_t> T;
+        for (size_t a : S) if (auts[a][v] == v) T.push_back(a);
+        S.swap(T);
+    }
+    p->sb_ok = true;
+}
+
 extern "C" int gm_plan_query(const gm_graph *g, uint32_t nq, uint32_t mq, const uint32_t *qedges,
                              const uint32_t *qlabels, const uint32_t *order, uint32_t filter,
                              void *stream_, gm_plan **out) {
@@ -235,6 +303,7 @@ extern "C" int gm_plan_query(const gm_graph *g, uint32_t nq, uint32_t mq, const 
             if (p->qadj[p->order[l]] >> p->order[i] & 1u) m |= 1u << i;
         p->bw[l] = m;
     }
+    symmetry_conditions(p);
     *out = p;
     return GM_OK;
 }
@@ -247,7 +316,9 @@ extern "C" int gm_plan_info(const gm_plan *p, gm_plan_info_t *info) {
         info->order[i] = p->order[i];
         info->backward[i] = p->bw[i];
         info->cand_count[i] = p->cand_count[i];
+        info->sb_conditions += (uint32_t)(__builtin_popcount(p->sb_gt[i]) + __builtin_popcount(p->sb_lt[i]));
     }
+    info->automorphisms = p->sb_ok ? p->aut : 0;
     return GM_OK;
 }
 

@@ -68,6 +68,8 @@ struct SearchParams {
     uint32_t candoff[kMaxQ];    // word offset of phi[l]'s candidate bitmap (phi[l] * words)
     uint32_t cand_needed;       // bit l: the filter of phi[l] is not implied by its backward edges
     uint32_t same_lab[kMaxQ];   // bit i of same_lab[l]: i < l and L(phi[i]) == L(phi[l])
+    uint32_t sb_gt[kMaxQ];      // symmetry breaking: bit i of sb_gt[l]: M[phi[l]] > M[phi[i]] required
+    uint32_t sb_lt[kMaxQ];      //                    bit i of sb_lt[l]: M[phi[l]] < M[phi[i]] required
     uint32_t walk_low[kMaxQ];   // lowest level process() must visit at level l (l if none)
     uint32_t col[kMaxQ];        // output column of position l (= phi[l])
     const uint32_t *pool;       // level-major, pool_size items of depth d0
@@ -209,12 +211,14 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     // Only levels holding a backward neighbour (adjacency check) or a vertex of v's label
     // (v can only collide with a same-label image) need visiting; the walk stops at the
     // deepest such level, uniformly across lanes (P.walk_low[l]).
-    const uint32_t eq = P.same_lab[l];
+    const uint32_t eq = P.same_lab[l], gt = P.sb_gt[l], lt = P.sb_lt[l];
     uint32_t p = src;
     int k = 0;
     for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
         const uint32_t w = S.v[i][p];
         if ((eq >> i) & 1u) ok = ok && (w != v);
+        if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
+        if ((lt >> i) & 1u) ok = ok && (v < w);
         if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
         p = S.pid[i][p];
     }
@@ -637,10 +641,12 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
             bool F = j < best;
             const uint32_t v = F ? ld_nc(P.nbr + cb + j) : 0;
             if (F) F = cand_bit(P, d, v, scratch);
+            const uint32_t gt = P.sb_gt[d], lt = P.sb_lt[d];
             for (uint32_t i = 0; i < d; ++i) {
                 const uint32_t mi = __shfl_sync(FULL, m, i);
-                const uint32_t loi = __shfl_sync(FULL, lo, i), hii = __shfl_sync(FULL, hi, i);
                 if (F && v == mi) F = false;
+                if (F && ((gt >> i) & 1u) && !(v > mi)) F = false;      // symmetry breaking
+                if (F && ((lt >> i) & 1u) && !(v < mi)) F = false;
                 if (F && ((checks >> i) & 1u)) F = has_edge(P, mi, lab, v, scratch);
             }
             const uint32_t fm = __ballot_sync(FULL, F);
@@ -837,6 +843,10 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     GM_CK(cudaEventCreate(&d0e)); GM_CK(cudaEventCreate(&d1e));
     GM_CK(cudaEventRecord(e0, st));
 
+    // symmetry breaking (count only): embeddings satisfying the plan's conditions, times |Aut(Q)|
+    const bool use_sb = !enumerate && p->sb_ok && p->aut > 1 && !(o.flags & GM_FLAG_NO_SYMMETRY);
+    rs.automorphisms = use_sb ? p->aut : 1;
+
     SearchParams P;
     memset(&P, 0, sizeof(P));
     P.offs = g->offs; P.nbr = g->nbr; P.cand = p->cand;
@@ -853,7 +863,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             P.cand_needed |= 1u << l;
         for (uint32_t i = 0; i < l; ++i)
             if (p->qlab[p->order[i]] == p->qlab[p->order[l]]) P.same_lab[l] |= 1u << i;
-        const uint32_t need = P.same_lab[l] | p->bw[l];
+        if (use_sb) { P.sb_gt[l] = p->sb_gt[l]; P.sb_lt[l] = p->sb_lt[l]; }
+        const uint32_t need = P.same_lab[l] | p->bw[l] | P.sb_gt[l] | P.sb_lt[l];
         P.walk_low[l] = need ? (uint32_t)__builtin_ctz(need) : l;
         P.col[l] = p->order[l];
     }
@@ -984,7 +995,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.limit_ns = o.time_limit_ms > 0 ? (unsigned long long)(o.time_limit_ms * 1e6) : 0ull;
         {   // last-level set counting applies when phi[last] has exactly one backward neighbour
             const uint32_t last = p->nq - 1, bwl = p->bw[last];
-            if (!enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && last >= 1 && __builtin_popcount(bwl) == 1) {
+            // (not when phi[last] carries symmetry-breaking bounds: those are checked per task)
+            if (!enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && last >= 1 && __builtin_popcount(bwl) == 1 &&
+                !(P.sb_gt[last] | P.sb_lt[last])) {
                 const uint32_t b = (uint32_t)__builtin_ctz(bwl);
                 P.bulk_last = 1;
                 P.last_b = b;
@@ -1024,6 +1037,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         rs.timed_out = h.abort ? 1 : 0;
         GM_CK(cudaEventElapsedTime(&rs.dfs_ms, d0e, d1e));
     }
+    if (use_sb) total *= p->aut;   // one embedding per Aut(Q)-orbit was counted
     // ---- outputs
     if (enumerate && mem == GM_MEM_HOST && enum_dev && cap) {
         const uint64_t rows = std::min<uint64_t>(cap, total);

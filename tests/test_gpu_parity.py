@@ -417,3 +417,40 @@ def test_hub_index_does_not_change_results(gm, seed):
         assert gm.gm_count(p, tau=1, set_count=False)[0] == ref
         rows, total, _ = gm.gm_enumerate(p, capacity=min(ref, 20000) + 1)
         assert total == ref
+
+
+def _aut_brute(q):
+    """|Aut(Q)|: label- and edge-preserving permutations, by brute force."""
+    import itertools
+    E = {(int(a), int(b)) for a, b in q.edges} | {(int(b), int(a)) for a, b in q.edges}
+    return sum(1 for pm in itertools.permutations(range(q.n))
+               if all(q.labels[pm[u]] == q.labels[u] for u in range(q.n))
+               and all((pm[a], pm[b]) in E for a, b in E))
+
+
+SYM_QUERIES = [gi.triangle(), gi.clique(4), gi.clique(5), gi.cycle(4), gi.cycle(5), gi.cycle(6), gi.star(3),
+               gi.path(4), gi.Query(3, [(0, 1), (1, 2), (0, 2)], [0, 0, 1]),
+               gi.Query(4, [(0, 1), (1, 2), (2, 3), (3, 0)], [0, 1, 0, 1]),
+               gi.Query(5, [(0, 1), (0, 2), (0, 3), (0, 4), (1, 2)], [0, 1, 1, 2, 2])]
+
+
+@pytest.mark.parametrize("qi", range(len(SYM_QUERIES)))
+def test_symmetry_breaking_counts(gm, qi):
+    """gm_count with symmetry breaking (one embedding per Aut(Q)-orbit, times |Aut(Q)|, as in
+    Appendix A) equals the oracle and the unbroken search; |Aut(Q)| equals brute force."""
+    q = SYM_QUERIES[qi]
+    nl = int(q.labels.max()) + 1
+    for seed in range(3):
+        n, s, d = (gi.rmat_edges(7, 6, seed) if seed % 2 == 0 else gi.er_edges(150, 9, seed))
+        lab = gi.uniform_labels(n, nl, seed)
+        og = OracleGraph(n, s, d, lab)
+        g = gm.gm_load_graph(n, s, d, lab, nl)
+        p = gm.gm_plan_query(g, q)
+        info = p.info()
+        assert info["automorphisms"] == _aut_brute(q)
+        ref = og.count(q)
+        for tau in (1, 10 ** 6):
+            c, st = gm.gm_count(p, tau=tau)
+            assert c == ref and st["automorphisms"] == info["automorphisms"]
+            assert gm.gm_count(p, tau=tau, symmetry=False)[0] == ref
+            assert gm.gm_count(p, tau=tau, set_count=False)[0] == ref
