@@ -125,7 +125,7 @@ static void ri_order(const gm_plan *p, uint32_t *order) {
 // symmetry breaking strategy in gMatch and T-DFS").  Aut(Q) = label- and edge-preserving
 // permutations of V(Q), enumerated by backtracking (given up above kMaxAut).  Conditions
 // are Grochow-Kellis: while the group is non-trivial, take the vertex v with the largest
-// orbit (earliest in phi on ties), require M[v] < M[w] for every other w of its orbit, and
+// orbit (earliest in phi on ties), require M[v] > M[w] for every other w of its orbit, and
 // continue with v's stabilizer.  Exactly one embedding of every Aut(Q)-orbit satisfies
 // them (the orbit of an embedding under Aut(Q) has |Aut(Q)| members, injectivity makes the
 // action free), so count = |Aut(Q)| * (embeddings satisfying the conditions).
@@ -177,10 +177,14 @@ static void symmetry_conditions(gm_plan *p) {
         const uint32_t v = (uint32_t)best;
         for (uint32_t w = 0; w < nq; ++w) {
             if (w == v || !((best_orbit >> w) & 1u)) continue;
-            // condition M[v] < M[w], checked when the later of the two is mapped
+            // condition M[v] > M[w] on device ids (the orbit representative is its largest
+            // image); device ids decrease with degree, so the earliest-ordered vertex is the
+            // lowest-degree image and its later orbit-mates are bounded to higher-degree
+            // (smaller) ids -- the degree-oriented DAG of triangle counting, generalised.
+            // Checked when the later of the two is mapped.
             const uint32_t lv = p->pos[v], lw = p->pos[w];
-            if (lv < lw) p->sb_gt[lw] |= 1u << lv;
-            else p->sb_lt[lv] |= 1u << lw;
+            if (lv < lw) p->sb_lt[lw] |= 1u << lv;   // at w's level: M[w] < M[v]
+            else p->sb_gt[lv] |= 1u << lw;           // at v's level: M[v] > M[w]
         }
         std::vector<size_t> T;
         for (size_t a : S) if (auts[a][v] == v) T.push_back(a);

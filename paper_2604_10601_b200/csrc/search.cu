@@ -118,6 +118,19 @@ __device__ __forceinline__ bool contains(const uint32_t *__restrict__ nbr, uint3
     return ld_nc(base) == v;
 }
 
+// Index of the first element >= x in the sorted a[0..n) (n if none).
+__device__ __forceinline__ uint32_t lower_bound_idx(const uint32_t *__restrict__ a, uint32_t n, uint32_t x,
+                                                    uint32_t &words) {
+    uint32_t lo = 0;
+    while (n > 0) {
+        const uint32_t half = n >> 1;
+        ++words;
+        if (ld_nc(a + lo + half) < x) { lo += half + 1; n -= half + 1; }
+        else n = half;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint32_t v, uint32_t &words) {
     if (!P.use_cand) return true;
     ++words;
@@ -167,17 +180,29 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
     if (valid) {
         const uint32_t bw = P.bw[l];
         const uint32_t lab = P.lab[l];
-        const int lowest = __ffs(bw) - 1;
+        const uint32_t gt = P.sb_gt[l], lt = P.sb_lt[l];
+        const int lowest = __ffs(bw | gt | lt) - 1;
         best = 0xffffffffu;
+        uint32_t lb = 0, ub = 0xffffffffu;     // symmetry breaking: candidates in [lb, ub)
         uint32_t p = lane;
         for (int i = l - 1; i >= lowest; --i) {
+            const uint32_t w = S.v[i][p];
             if ((bw >> i) & 1u) {
-                const uint32_t row = S.v[i][p] * P.S + lab;
+                const uint32_t row = w * P.S + lab;
                 const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
                 words += 2;
                 if (hi - lo < best) { best = hi - lo; cb = lo; cs = (uint32_t)i; }
             }
+            if ((gt >> i) & 1u) lb = max(lb, w + 1);
+            if ((lt >> i) & 1u) ub = min(ub, w);
             p = S.pid[i][p];
+        }
+        if (gt | lt) {   // the slice is sorted: cut it to the ids the conditions allow
+            uint32_t a = 0, e = best;
+            if (lb > 0 && best) a = lower_bound_idx(P.nbr + cb, best, lb, words);
+            if (ub != 0xffffffffu && best) e = lower_bound_idx(P.nbr + cb, best, ub, words);
+            cb += a;
+            best = e > a ? e - a : 0;
         }
     }
     S.cb[l][lane] = cb;
@@ -634,8 +659,29 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
             const uint32_t ob = __shfl_xor_sync(FULL, best, o), oll = __shfl_xor_sync(FULL, bl, o);
             if (ob < best || (ob == best && oll > bl)) { best = ob; bl = oll; }
         }
-        const uint32_t cb = __shfl_sync(FULL, lo, bl);
+        uint32_t cb = __shfl_sync(FULL, lo, bl);
         const uint32_t checks = bw & ~(1u << bl);
+        {   // symmetry breaking: cut the sorted slice to [lb, ub) (see generate)
+            const uint32_t gtm = P.sb_gt[d], ltm = P.sb_lt[d];
+            if (gtm | ltm) {
+                uint32_t lb = (lane < d && ((gtm >> lane) & 1u)) ? m + 1 : 0u;
+                uint32_t ub = (lane < d && ((ltm >> lane) & 1u)) ? m : 0xffffffffu;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    lb = max(lb, __shfl_xor_sync(FULL, lb, o));
+                    ub = min(ub, __shfl_xor_sync(FULL, ub, o));
+                }
+                uint32_t a = 0, e = best;
+                if (lane == 0 && best) {
+                    if (lb > 0) a = lower_bound_idx(P.nbr + cb, best, lb, scratch);
+                    if (ub != 0xffffffffu) e = lower_bound_idx(P.nbr + cb, best, ub, scratch);
+                }
+                a = __shfl_sync(FULL, a, 0);
+                e = __shfl_sync(FULL, e, 0);
+                cb += a;
+                best = e > a ? e - a : 0;
+            }
+        }
         for (uint32_t j0 = 0; j0 < best; j0 += 32) {
             const uint32_t j = j0 + lane;
             bool F = j < best;
