@@ -163,7 +163,8 @@ GM_API void gm_free_plan(gm_plan *p);
                                     (Alg. 2 as written) instead of set-counting the last level
                                     when phi[last] has a single backward neighbour */
 #define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
-                                    Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)| */
+                                    Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)|.
+                                    Symmetry breaking is also skipped when `roots` is given. */
 
 typedef struct {
     uint64_t tau;            /* initial task-pool threshold (§4.3); 0 = 1e6 */

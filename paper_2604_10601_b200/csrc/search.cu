@@ -748,7 +748,6 @@ __global__ void k_write_single(const uint32_t *__restrict__ roots, unsigned long
         out[i] = new2old[roots[i]];
 }
 
-__global__ void k_read_timer(unsigned long long *t) { *t = globaltimer(); }
 
 __global__ void k_init_ring(unsigned long long *seq, unsigned long long cap) {
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < cap;
@@ -889,8 +888,16 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     GM_CK(cudaEventCreate(&d0e)); GM_CK(cudaEventCreate(&d1e));
     GM_CK(cudaEventRecord(e0, st));
 
-    // symmetry breaking (count only): embeddings satisfying the plan's conditions, times |Aut(Q)|
-    const bool use_sb = !enumerate && p->sb_ok && p->aut > 1 && !(o.flags & GM_FLAG_NO_SYMMETRY);
+    // symmetry breaking (count only): embeddings satisfying the plan's conditions, times |Aut(Q)|.
+    // Not when a condition would land on phi[last] while last-level set counting applies
+    // (one backward neighbour): set counting saves far more than the |Aut| factor there.
+    const bool set_count_ok = !enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && p->nq >= 2 &&
+                              __builtin_popcount(p->bw[p->nq - 1]) == 1;
+    // Also not with a user root list: "embeddings whose root is in the list" is not a union of
+    // Aut(Q)-orbits.  (A rank partition is fine: every orbit representative has one root, so
+    // the ranks' representative counts add up to the full one.)
+    const bool use_sb = !enumerate && p->sb_ok && p->aut > 1 && !(o.flags & GM_FLAG_NO_SYMMETRY) && !o.roots &&
+                        !(set_count_ok && (p->sb_gt[p->nq - 1] | p->sb_lt[p->nq - 1]));
     rs.automorphisms = use_sb ? p->aut : 1;
 
     SearchParams P;

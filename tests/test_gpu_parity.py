@@ -451,6 +451,7 @@ def test_symmetry_breaking_counts(gm, qi):
         ref = og.count(q)
         for tau in (1, 10 ** 6):
             c, st = gm.gm_count(p, tau=tau)
-            assert c == ref and st["automorphisms"] == info["automorphisms"]
+            # symmetry breaking is used unless it would disable last-level set counting
+            assert c == ref and st["automorphisms"] in (1, info["automorphisms"])
             assert gm.gm_count(p, tau=tau, symmetry=False)[0] == ref
             assert gm.gm_count(p, tau=tau, set_count=False)[0] == ref
