@@ -346,6 +346,7 @@ def main():
             timeouts += st["timed_out"]
             if k == 0:
                 per_query.append({"q": qs[i].name, "m": int(len(qs[i].edges)), "ms": round(q_ms[-1], 3),
+                                  "embeddings": int(counts_dev[i].item()), "aut": st["automorphisms"],
                                   "dfs_ms": round(st["dfs_ms"], 3), "timed_out": st["timed_out"],
                                   "pool": st["pool_size"], "depth": st["pool_depth"],
                                   "donations": st["donations"]})

@@ -532,36 +532,47 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
 
             // ---- ScatterTask, warp-parallel: next 32 tasks of the virtual task pool at level l
             const uint32_t ci = S.ci[l], cj = S.cj[l];
-            uint32_t rem = 0;
-            if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
-            const uint32_t r32 = min(rem, 32u);
-            uint32_t incl = r32;
+            uint32_t src, off, k;
+            const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
+            if (cl_ci - cj >= 32 && ci < 32) {
+                // fast path: the cursor's slice alone fills the batch (long slices, hubs)
+                src = ci; off = cj + lane; k = 32;
+                if (lane == 0) {
+                    if (cj + 32 < cl_ci) S.cj[l] = cj + 32;
+                    else { S.ci[l] = ci + 1; S.cj[l] = 0; }
+                }
+            } else {
+                uint32_t rem = 0;
+                if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
+                const uint32_t r32 = min(rem, 32u);
+                uint32_t incl = r32;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t x = __shfl_up_sync(FULL, incl, o);
-                if (lane >= (uint32_t)o) incl += x;
-            }
-            const uint32_t total = __shfl_sync(FULL, incl, 31);
-            if (total == 0) { --l; continue; }       // level exhausted: backtrack
-            const uint32_t k = min(total, 32u);
-            // source lane of task `lane` = number of lanes whose inclusive count is <= lane
-            uint32_t src = 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t x = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= (uint32_t)o) incl += x;
+                }
+                const uint32_t total = __shfl_sync(FULL, incl, 31);
+                if (total == 0) { --l; continue; }       // level exhausted: backtrack
+                k = min(total, 32u);
+                // source lane of task `lane` = number of lanes whose inclusive count is <= lane
+                src = 0;
 #pragma unroll
-            for (uint32_t b = 16; b >= 1; b >>= 1) {
-                const uint32_t x = __shfl_sync(FULL, incl, src + b - 1);
-                if (x <= lane) src += b;
+                for (uint32_t b = 16; b >= 1; b >>= 1) {
+                    const uint32_t x = __shfl_sync(FULL, incl, src + b - 1);
+                    if (x <= lane) src += b;
+                }
+                src = min(src, 31u);
+                const uint32_t src_excl = __shfl_sync(FULL, incl - r32, src);
+                off = lane < k ? lane - src_excl + (src == ci ? cj : 0) : 0;
+                const uint32_t lsrc = __shfl_sync(FULL, src, k - 1);
+                const uint32_t loff = __shfl_sync(FULL, off, k - 1);
+                if (lane == 0) {
+                    if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
+                    else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
+                }
             }
-            src = min(src, 31u);
-            const uint32_t src_excl = __shfl_sync(FULL, incl - r32, src);
             const bool has = lane < k;
-            const uint32_t off = has ? lane - src_excl + (src == ci ? cj : 0) : 0;
             const uint32_t v = has ? ld_nc(P.nbr + S.cb[l][src] + off) : 0;
-            const uint32_t lsrc = __shfl_sync(FULL, src, k - 1);
-            const uint32_t loff = __shfl_sync(FULL, off, k - 1);
-            if (lane == 0) {
-                if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
-                else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
-            }
             my_rounds += (lane == 0);
             my_tasks += has;
 
