@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgmatch.so")
+LIB_PATH = os.environ.get("GM_LIB") or os.path.join(_HERE, "libgmatch.so")   # GM_LIB: A/B builds
 
 GM_OK, GM_ERR_ARG, GM_ERR_CUDA, GM_ERR_NOMEM, GM_ERR_LIMIT, GM_TIMEOUT = 0, 1, 2, 3, 4, 5
 GM_MEM_HOST, GM_MEM_DEVICE = 0, 1

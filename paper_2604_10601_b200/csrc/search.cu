@@ -237,18 +237,21 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     // (v can only collide with a same-label image) need visiting; the walk stops at the
     // deepest such level, uniformly across lanes (P.walk_low[l]).
     const uint32_t eq = P.same_lab[l], gt = P.sb_gt[l], lt = P.sb_lt[l];
+    const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
     uint32_t p = src;
-    int k = 0;
+    int kh = 0, kn = nchk - 1;                      // hub checks first (one load), searches last
     for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
         const uint32_t w = S.v[i][p];
         if ((eq >> i) & 1u) ok = ok && (w != v);
         if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
         if ((lt >> i) & 1u) ok = ok && (v < w);
-        if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
+        if (has && ((chk >> i) & 1u)) {              // (exactly nchk bits when has)
+            if (w < P.nhubs) { S.chk[kh][lane] = w; ++kh; }
+            else { S.chk[kn][lane] = w; --kn; }
+        }
         p = S.pid[i][p];
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
-    const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
     // Two checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
     // independent, so each lane keeps two dependent-load chains in flight (ncu: the kernel
     // is bound by long-scoreboard stalls on L2-resident probes, not by bandwidth).

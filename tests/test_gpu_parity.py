@@ -419,6 +419,20 @@ def test_hub_index_does_not_change_results(gm, seed):
         assert total == ref
 
 
+def test_symmetry_breaking_at_scale(gm):
+    """R-MAT scale 16 (65k vertices, 1M edges): symmetric patterns counted with symmetry
+    breaking + id-range slice cuts equal the full search (different code path, same library)
+    and, on sampled roots, the oracle (test_symmetry_breaking_counts pins the small cases)."""
+    n, s, d = gi.rmat_edges(16, 16, 21)
+    g = gm.gm_load_graph(n, s, d)
+    for q in (gi.triangle(), gi.clique(4), gi.cycle(4)):
+        p = gm.gm_plan_query(g, q)
+        c_sb, st = gm.gm_count(p)
+        c_full, st2 = gm.gm_count(p, symmetry=False)
+        assert st["automorphisms"] > 1 and st2["automorphisms"] == 1
+        assert c_sb == c_full and c_sb > 0
+
+
 def _aut_brute(q):
     """|Aut(Q)|: label- and edge-preserving permutations, by brute force."""
     import itertools

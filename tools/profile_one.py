@@ -17,9 +17,13 @@ cfgname = sys.argv[3] if len(sys.argv) > 3 else "rmat18"
 tau = int(float(sys.argv[4])) if len(sys.argv) > 4 else 1000000
 cfg = bench.CONFIGS[cfgname]
 n, s, d, lab = bench.make_graph_device(cfg)
-sh, dh, lh = (x.cpu().numpy().view(np.uint32) for x in (s, d, lab))
-off, nb = gi.simple_adjacency(n, sh, dh)
-qs = bench.build_queries(cfg, gi.HostAdjacency(off, nb), lh)
+lh = lab.cpu().numpy().view(np.uint32)
+if cfg.get("dense") or cfg.get("sparse"):
+    import gminputs.gpu as gg
+    adj = gg.DeviceNeighbors(n, s, d)
+else:
+    adj = None                      # fixed patterns only
+qs = bench.build_queries(cfg, adj, lh)
 g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
 q = qs[qi]
 p = gm.gm_plan_query(g, q)
