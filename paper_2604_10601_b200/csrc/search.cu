@@ -239,16 +239,15 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     const uint32_t eq = P.same_lab[l], gt = P.sb_gt[l], lt = P.sb_lt[l];
     const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
     uint32_t p = src;
-    int kh = 0, kn = nchk - 1;                      // hub checks first (one load), searches last
+    int k = 0;
+    // (ordering hub checks first measured 1-7 % slower on rmat18 dense queries: pairs of
+    // mixed hub/search probes overlap better)
     for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
         const uint32_t w = S.v[i][p];
         if ((eq >> i) & 1u) ok = ok && (w != v);
         if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
         if ((lt >> i) & 1u) ok = ok && (v < w);
-        if (has && ((chk >> i) & 1u)) {              // (exactly nchk bits when has)
-            if (w < P.nhubs) { S.chk[kh][lane] = w; ++kh; }
-            else { S.chk[kn][lane] = w; --kn; }
-        }
+        if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
         p = S.pid[i][p];
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
