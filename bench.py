@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--time-limit-ms", type=float, default=None)
     ap.add_argument("--tau", type=float, default=1e6)
     ap.add_argument("--no-steal", action="store_true")
+    ap.add_argument("--static-roots", action="store_true",
+                    help="N > 1: static (v/64) %% N root partition instead of the shared pool counter")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-query", action="store_true", help="print per-query timings to stderr")
     args = ap.parse_args()
@@ -293,6 +295,17 @@ def main():
     ginfo = g.info()
     stream = torch.cuda.current_stream()
     run_kw = dict(tau=int(args.tau), rank=rank, world=world, steal=not args.no_steal, time_limit_ms=limit)
+    # N > 1: dynamic chunk assignment -- every rank's DFS claims pool batches from ONE counter
+    # in rank 0's memory (CUDA IPC + NVLink peer atomics); --static-roots: (v/64) % N partition
+    shared_ptr = None
+    if world > 1 and not args.static_roots:
+        if rank == 0:
+            shared_ptr, handle = gm.gm_pool_counter_create()
+        box = [handle if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        if rank != 0:
+            shared_ptr = gm.gm_pool_counter_open(box[0])
+        run_kw = dict(tau=int(args.tau), steal=not args.no_steal, time_limit_ms=limit, shared_pool_ctr=shared_ptr)
 
     counts_dev = torch.zeros(len(qs), dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -305,7 +318,14 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             p = gm.gm_plan_query(g, q, filter="nlf")
+            if shared_ptr is not None:          # reset the shared counter, then start together
+                if rank == 0:
+                    gm.gm_pool_counter_reset(shared_ptr)
+                torch.cuda.synchronize()
+                dist.barrier()
             _, st = gm.gm_count(p, out=counts_dev[i:i + 1], **run_kw)
+            if shared_ptr is not None:
+                dist.barrier()                  # nobody resets while another rank still searches
             e1.record(stream)
             plans.append(p)
             out.append((st, e0, e1))
@@ -376,7 +396,14 @@ def main():
         local = []
         for q in qs:
             p = gm.gm_plan_query(g, q, filter="nlf")      # query arrays copied H2D by the library
+            if shared_ptr is not None:
+                if rank == 0:
+                    gm.gm_pool_counter_reset(shared_ptr)
+                torch.cuda.synchronize()
+                dist.barrier()
             c, _ = gm.gm_count(p, **run_kw)                # count read back D2H
+            if shared_ptr is not None:
+                dist.barrier()
             local.append(c)
             h2d += q.edges.nbytes + q.labels.nbytes
             d2h += 8
@@ -424,7 +451,10 @@ def main():
                    "embeddings_per_step": emb_per_step, "tau": int(args.tau), "steal": not args.no_steal,
                    "filter": "nlf", "graph": {k: ginfo[k] for k in ("n", "num_adj", "num_labels", "d_max")},
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"roots split over {world} GPU(s), CSR replicated, 1 NCCL all-reduce/step"},
+                   "parallelism": (f"{world} GPU(s), CSR replicated, " +
+                                   ("pool batches claimed from one shared counter (NVLink peer atomics)"
+                                    if shared_ptr is not None else "static root partition") +
+                                   ", 1 all-reduce of the counts per step")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_dfs", "launch_ms_mean": dfs_launch_ms,

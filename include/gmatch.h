@@ -181,6 +181,11 @@ typedef struct {
     uint64_t num_roots;
     uint64_t pool_bytes_max; /* cap on the BFS pool's device bytes; 0 = 1 GiB */
     uint32_t flags;          /* GM_FLAG_* bits */
+    void    *shared_pool_ctr;/* optional device pointer to a pool counter shared by several
+                                ranks (gm_pool_counter_*): every rank then builds the SAME
+                                initial pool (rank/world are ignored) and their DFS kernels
+                                claim pool batches from this one counter -- dynamic chunk
+                                assignment across GPUs through NVLink peer atomics */
 } gm_run_opts;
 
 GM_API void gm_default_opts(gm_run_opts *o);
@@ -223,6 +228,28 @@ GM_API int gm_count(const gm_plan *p, const gm_run_opts *opts, uint64_t *count_o
  */
 GM_API int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t *out, uint64_t capacity,
                  int mem, uint64_t *count_host, gm_run_stats *stats, void *stream);
+
+/* ------------------------------------------------------------------ multi-GPU pool counter */
+
+/*
+ * A 64-bit counter in one GPU's memory that the DFS kernels of several ranks (processes, one
+ * per GPU) atomically claim pool batches from, over NVLink peer memory -- the north_star's
+ * "root-level candidates ... partitioned across the 8 GPUs with dynamic chunk assignment".
+ *   gm_pool_counter_create: allocate it on the current device (zeroed); copies a
+ *       GM_IPC_HANDLE_BYTES CUDA IPC handle into ipc_handle_out for the other ranks.
+ *   gm_pool_counter_open:   map another process's counter (any GPU of the node, or the
+ *       same GPU) into this process; *counter_dev is then usable as shared_pool_ctr.
+ *   gm_pool_counter_reset:  set it to 0 on `stream` (call on one rank before each search).
+ *   gm_pool_counter_close:  owner = 1 frees the allocation, owner = 0 unmaps it.
+ * Protocol: reset on one rank, synchronize all ranks (barrier), run gm_count on every rank
+ * with the same plan inputs and shared_pool_ctr set, synchronize again before the next reset;
+ * sum the per-rank counts (one all-reduce).
+ */
+#define GM_IPC_HANDLE_BYTES 64
+GM_API int gm_pool_counter_create(void **counter_dev, void *ipc_handle_out);
+GM_API int gm_pool_counter_open(const void *ipc_handle, void **counter_dev);
+GM_API int gm_pool_counter_reset(void *counter_dev, void *stream);
+GM_API int gm_pool_counter_close(void *counter_dev, int owner);
 
 /* Thread-local description of the last error (empty string if none). */
 GM_API const char *gm_last_error(void);

@@ -177,7 +177,8 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
-          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True):
+          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True,
+          shared_pool_ctr=None):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -203,7 +204,33 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.flags |= L.GM_FLAG_NO_SET_COUNT
     if not symmetry:
         o.flags |= L.GM_FLAG_NO_SYMMETRY
+    if shared_pool_ctr is not None:
+        o.shared_pool_ctr = ctypes.c_void_p(int(shared_pool_ctr))
     return o, keep
+
+
+def gm_pool_counter_create():
+    """(device pointer, IPC handle bytes) of a new cross-rank pool counter on this GPU."""
+    ptr = ctypes.c_void_p(0)
+    h = (ctypes.c_char * L.GM_IPC_HANDLE_BYTES)()
+    L.check(L.lib().gm_pool_counter_create(ctypes.byref(ptr), h))
+    return ptr.value, bytes(h)
+
+
+def gm_pool_counter_open(handle: bytes):
+    """Map another rank's pool counter; returns its device pointer in this process."""
+    ptr = ctypes.c_void_p(0)
+    buf = (ctypes.c_char * L.GM_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    L.check(L.lib().gm_pool_counter_open(buf, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def gm_pool_counter_reset(ptr, stream=None):
+    L.check(L.lib().gm_pool_counter_reset(ctypes.c_void_p(ptr), _stream_handle(stream)))
+
+
+def gm_pool_counter_close(ptr, owner: bool):
+    L.check(L.lib().gm_pool_counter_close(ctypes.c_void_p(ptr), 1 if owner else 0))
 
 
 def gm_count(p: Plan, out=None, stream=None, **kw):

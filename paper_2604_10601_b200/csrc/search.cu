@@ -31,6 +31,10 @@
 
 #include <algorithm>
 #include <mutex>
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <vector>
 
 #include "gm_internal.cuh"
@@ -78,6 +82,7 @@ struct SearchParams {
     uint32_t steal;
     Ctrl *ctrl;
     uint32_t batch;             // pool items fetched per warp (<= 32)
+    unsigned long long *pool_ctr;  // &ctrl->pool_ctr, or a counter shared across ranks
     uint32_t *q_items;          // q_cap * kItemWords
     unsigned long long *q_seq;  // q_cap per-slot sequence numbers (Vyukov bounded MPMC ring)
     unsigned long long q_cap;
@@ -392,9 +397,11 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
             if (lane == 0) {
                 if (VC->abort) {
                     exit_now = 1;
-                } else if (VC->pool_ctr < P.pool_size) {
+                } else if (*(volatile unsigned long long *)P.pool_ctr < P.pool_size) {
                     atomicAdd(&C->work, 1);
-                    b = atomicAdd(&C->pool_ctr, (unsigned long long)P.batch);
+                    // P.pool_ctr: this launch's counter, or one shared by every rank's launch
+                    // (peer memory over NVLink: multi-GPU dynamic chunk assignment)
+                    b = atomicAdd(P.pool_ctr, (unsigned long long)P.batch);
                     if (b >= P.pool_size) { atomicSub(&C->work, 1); b = ~0ull; }
                 }
                 if (!exit_now && b == ~0ull) {
@@ -406,7 +413,9 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
                         const unsigned long long pos = VC->q_head;
                         const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
                         if (seq == pos + 1 && atomicCAS(&C->q_head, pos, pos + 1) == pos) item = pos;
-                        if (item == ~0ull && VC->pool_ctr >= P.pool_size && VC->work == 0) exit_now = 1;
+                        if (item == ~0ull && *(volatile unsigned long long *)P.pool_ctr >= P.pool_size &&
+                            VC->work == 0)
+                            exit_now = 1;
                     }
                 }
                 if (b != ~0ull || item != ~0ull) registered = false;
@@ -645,13 +654,17 @@ __global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
 // ------------------------------------------------------------------ BFS expansion
 
 // One warp per partial match of depth d (level-major input).  MODE 0: count children
-// into ctrl->count.  MODE 1: write children (depth d+1, level-major, stride out_stride).
-// MODE 2: write children as final enumerate rows (by query-vertex column).
+// into *ctr (and, if item_off, each item's child count into item_off[item]).  MODE 1: write
+// children (depth d+1, level-major, stride out_stride) -- at item_off[item] + rank within the
+// item when item_off is given (the exclusive scan of MODE 0's counts: a deterministic pool,
+// identical on every rank), else at atomically claimed positions.  MODE 2: write children
+// as final enumerate rows (by query-vertex column).
 template <int MODE>
 __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint32_t *__restrict__ in,
                                                 unsigned long long nin, uint32_t d, uint32_t *__restrict__ outp,
                                                 unsigned long long out_stride, unsigned long long out_cap,
-                                                unsigned long long *__restrict__ ctr) {
+                                                unsigned long long *__restrict__ ctr,
+                                                unsigned long long *__restrict__ item_off) {
     const uint32_t lane = threadIdx.x & 31;
     const unsigned long long warp = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
@@ -695,6 +708,8 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
                 best = e > a ? e - a : 0;
             }
         }
+        unsigned long long item_base = 0, item_cnt = 0;
+        if (MODE == 1 && item_off) item_base = item_off[it];
         for (uint32_t j0 = 0; j0 < best; j0 += 32) {
             const uint32_t j = j0 + lane;
             bool F = j < best;
@@ -711,10 +726,16 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
             const uint32_t fm = __ballot_sync(FULL, F);
             if (MODE == 0) {
                 local += __popc(fm);
+                item_cnt += __popc(fm);
             } else if (fm) {
                 unsigned long long basepos = 0;
-                if (lane == 0) basepos = atomicAdd(ctr, (unsigned long long)__popc(fm));
-                basepos = __shfl_sync(FULL, basepos, 0);
+                if (MODE == 1 && item_off) {
+                    basepos = item_base + item_cnt;
+                    item_cnt += __popc(fm);
+                } else {
+                    if (lane == 0) basepos = atomicAdd(ctr, (unsigned long long)__popc(fm));
+                    basepos = __shfl_sync(FULL, basepos, 0);
+                }
                 const unsigned long long pos = basepos + __popc(fm & ((1u << lane) - 1));
                 const bool wr = F && pos < out_cap;
                 for (uint32_t i = 0; i < d; ++i) {
@@ -730,6 +751,7 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
                 }
             }
         }
+        if (MODE == 0 && item_off && lane == 0) item_off[it] = item_cnt;
     }
     if (MODE == 0 && lane == 0 && local) atomicAdd(ctr, local);
 }
@@ -737,22 +759,23 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
 // Root candidates owned by this rank: cand bit of phi[0] set and (o / chunk) % world == rank
 // for the ORIGINAL id o (ownership is defined on the caller's ids; device ids are degree-
 // ordered and would put all hubs on one rank).  User roots arrive as original ids.
-__global__ void k_roots(const SearchParams P, unsigned long long n, const uint32_t *__restrict__ user,
-                        unsigned long long nuser, uint32_t rank, uint32_t world, uint32_t chunk,
-                        uint32_t *__restrict__ out, unsigned long long *__restrict__ ctr,
-                        const uint32_t *__restrict__ vlab) {
-    const unsigned long long total = user ? nuser : n;
-    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long o = user ? user[i] : P.new2old[i];
-        bool ok = o < n && (o / chunk) % world == rank;
-        if (!ok) continue;
-        const uint32_t v = user ? P.old2new[o] : (uint32_t)i;
-        uint32_t scratch = 0;
-        ok = vlab[v] == P.lab[0] && cand_bit(P, 0, v, scratch);
-        if (ok) out[atomicAdd(ctr, 1ull)] = v;
+// Selected with a stable device-wide select, so the root list -- and the BFS pool built
+// from it -- is identical run to run and rank to rank (needed by the shared pool counter).
+struct RootSel {
+    const uint32_t *cand, *vlab, *new2old, *old2new, *user;
+    unsigned long long n;
+    uint32_t candoff, lab0, rank, world, chunk;
+    __device__ uint32_t operator()(unsigned long long i) const {
+        const unsigned long long o = user ? user[i] : new2old[i];
+        if (o >= n || (o / chunk) % world != rank) return 0xffffffffu;
+        const uint32_t v = user ? old2new[o] : (uint32_t)i;
+        if (vlab[v] != lab0 || !((cand[candoff + (v >> 5)] >> (v & 31)) & 1u)) return 0xffffffffu;
+        return v;
     }
-}
+};
+struct NotNone {
+    __device__ bool operator()(uint32_t x) const { return x != 0xffffffffu; }
+};
 
 __global__ void k_write_single(const uint32_t *__restrict__ roots, unsigned long long n, uint32_t *__restrict__ out,
                                unsigned long long cap, const uint32_t *__restrict__ new2old) {
@@ -777,9 +800,14 @@ struct Workspace {
     unsigned long long q_cap = 0;
     uint32_t *buf[2] = {nullptr, nullptr};
     size_t buf_bytes[2] = {0, 0};
+    uint32_t *tmp = nullptr;        // CUB scratch
+    size_t tmp_bytes = 0;
+    uint32_t *item_off = nullptr;   // per-item child counts / offsets of a BFS level (u64)
+    size_t item_off_bytes = 0;
     int sms = 148;
     ~Workspace() {
         cudaFree(ctrl); cudaFree(q_items); cudaFree(q_seq); cudaFree(buf[0]); cudaFree(buf[1]);
+        cudaFree(tmp); cudaFree(item_off);
     }
 };
 
@@ -956,10 +984,20 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         GM_CK(cudaMemcpyAsync(d_user, o.roots, sizeof(uint32_t) * o.num_roots, cudaMemcpyHostToDevice, st));
     }
     if (nroot_cap) {
-        k_roots<<<grid_for(nroot_cap, 256, W.sms), 256, 0, st>>>(P, g->n, d_user, o.num_roots, o.rank, o.world,
-                                                                  o.root_chunk, W.buf[0], ctr_aux, g->lab);
-        GM_CK(cudaGetLastError());
-        ++launches;
+        RootSel sel;
+        sel.cand = p->cand; sel.vlab = g->lab; sel.new2old = g->new2old; sel.old2new = g->old2new;
+        sel.user = d_user; sel.n = g->n; sel.candoff = P.candoff[0]; sel.lab0 = P.lab[0];
+        // with a shared pool counter every rank builds the SAME (whole) pool
+        sel.rank = o.shared_pool_ctr ? 0 : o.rank;
+        sel.world = o.shared_pool_ctr ? 1 : o.world;
+        sel.chunk = o.root_chunk;
+        auto items = thrust::make_transform_iterator(thrust::counting_iterator<unsigned long long>(0), sel);
+        size_t tb = 0;
+        GM_CK(cub::DeviceSelect::If(nullptr, tb, items, W.buf[0], ctr_aux, (int64_t)nroot_cap, NotNone(), st));
+        rc = ensure(W.tmp, W.tmp_bytes, tb + 16);
+        if (rc) return rc;
+        GM_CK(cub::DeviceSelect::If(W.tmp, tb, items, W.buf[0], ctr_aux, (int64_t)nroot_cap, NotNone(), st));
+        launches += 1;
     }
     unsigned long long nroots = 0;
     GM_CK(cudaMemcpyAsync(&nroots, ctr_aux, sizeof(nroots), cudaMemcpyDeviceToHost, st));
@@ -1004,7 +1042,14 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         if (P_n >= o.tau) break;
         GM_CK(cudaMemcpyAsync(ctr_count, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
         const int gb = grid_for(P_n * 32, 256, W.sms);
-        k_expand<0><<<gb, 256, 0, st>>>(P, frontier, P_n, d, nullptr, 0, 0, ctr_count);
+        const bool last_level = d + 1 == p->nq;
+        unsigned long long *item_off = nullptr;
+        if (!last_level) {   // per-item counts -> offsets: a deterministic next level
+            rc = ensure(W.item_off, W.item_off_bytes, sizeof(unsigned long long) * P_n);
+            if (rc) return rc;
+            item_off = reinterpret_cast<unsigned long long *>(W.item_off);
+        }
+        k_expand<0><<<gb, 256, 0, st>>>(P, frontier, P_n, d, nullptr, 0, 0, ctr_count, item_off);
         GM_CK(cudaGetLastError());
         ++launches;
         unsigned long long c = 0;
@@ -1014,7 +1059,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             total = c;
             if (enumerate && c && cap) {
                 GM_CK(cudaMemcpyAsync(ctr_aux, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
-                k_expand<2><<<gb, 256, 0, st>>>(P, frontier, P_n, d, out_dev(), 0, cap, ctr_aux);
+                k_expand<2><<<gb, 256, 0, st>>>(P, frontier, P_n, d, out_dev(), 0, cap, ctr_aux, nullptr);
                 GM_CK(cudaGetLastError());
                 ++launches;
             }
@@ -1026,8 +1071,15 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         if (need > o.pool_bytes_max) break;
         rc = ensure(W.buf[cur ^ 1], W.buf_bytes[cur ^ 1], need);
         if (rc) return rc;
-        GM_CK(cudaMemcpyAsync(ctr_aux, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
-        k_expand<1><<<gb, 256, 0, st>>>(P, frontier, P_n, d, W.buf[cur ^ 1], c, c, ctr_aux);
+        {   // exclusive scan of the per-item counts (in place)
+            size_t tb = 0;
+            GM_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, item_off, item_off, (int64_t)P_n, st));
+            rc = ensure(W.tmp, W.tmp_bytes, tb + 16);
+            if (rc) return rc;
+            GM_CK(cub::DeviceScan::ExclusiveSum(W.tmp, tb, item_off, item_off, (int64_t)P_n, st));
+            ++launches;
+        }
+        k_expand<1><<<gb, 256, 0, st>>>(P, frontier, P_n, d, W.buf[cur ^ 1], c, c, ctr_aux, item_off);
         GM_CK(cudaGetLastError());
         ++launches;
         cur ^= 1;
@@ -1052,6 +1104,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         }
         GM_CK(cudaMemsetAsync(W.ctrl, 0, sizeof(Ctrl), st));
         P.pool = frontier;
+        P.pool_ctr = o.shared_pool_ctr ? reinterpret_cast<unsigned long long *>(o.shared_pool_ctr)
+                                       : &W.ctrl->pool_ctr;
         P.pool_size = P_n;
         P.d0 = d;
         P.steal = o.steal ? 1 : 0;
@@ -1135,4 +1189,45 @@ extern "C" int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t 
                             uint64_t *count_host, gm_run_stats *stats, void *stream) {
     GM_REQ(capacity == 0 || out, GM_ERR_ARG, "gm_enumerate: out NULL with capacity > 0");
     return run_search(p, opts, true, out, capacity, mem, count_host, GM_MEM_HOST, stats, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ multi-GPU pool counter
+
+extern "C" int gm_pool_counter_create(void **counter_dev, void *ipc_handle_out) {
+    set_error("");
+    GM_REQ(counter_dev && ipc_handle_out, GM_ERR_ARG, "gm_pool_counter_create: NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) <= GM_IPC_HANDLE_BYTES, "IPC handle size");
+    void *p = nullptr;
+    GM_CK(cudaMalloc(&p, 256));                 // own 256-byte block: the counter's line alone
+    GM_CK(cudaMemset(p, 0, 256));
+    cudaIpcMemHandle_t h;
+    GM_CK(cudaIpcGetMemHandle(&h, p));
+    memset(ipc_handle_out, 0, GM_IPC_HANDLE_BYTES);
+    memcpy(ipc_handle_out, &h, sizeof(h));
+    *counter_dev = p;
+    return GM_OK;
+}
+
+extern "C" int gm_pool_counter_open(const void *ipc_handle, void **counter_dev) {
+    set_error("");
+    GM_REQ(counter_dev && ipc_handle, GM_ERR_ARG, "gm_pool_counter_open: NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    void *p = nullptr;
+    GM_CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *counter_dev = p;
+    return GM_OK;
+}
+
+extern "C" int gm_pool_counter_reset(void *counter_dev, void *stream) {
+    GM_REQ(counter_dev, GM_ERR_ARG, "gm_pool_counter_reset: NULL counter");
+    GM_CK(cudaMemsetAsync(counter_dev, 0, sizeof(unsigned long long), (cudaStream_t)stream));
+    return GM_OK;
+}
+
+extern "C" int gm_pool_counter_close(void *counter_dev, int owner) {
+    if (!counter_dev) return GM_OK;
+    if (owner) GM_CK(cudaFree(counter_dev));
+    else GM_CK(cudaIpcCloseMemHandle(counter_dev));
+    return GM_OK;
 }

@@ -1,0 +1,87 @@
+"""Multi-rank GPU paths (2 processes; they share GPU 0 when the box has one): the static root
+partition and the cross-rank shared pool counter (CUDA IPC + peer atomics) both give per-rank
+counts that sum, with one all-reduce, to the single-rank count and to the oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import gminputs as gi
+        import paper_2604_10601_b200 as gm
+        n, s, d = gi.rmat_edges(11, 8, 13)
+        lab = gi.uniform_labels(n, 3, 13)
+        g = gm.gm_load_graph(n, s, d, lab, 3)
+        queries = [gi.tailed_triangle((0, 1, 2, 0)), gi.Query(4, [(0, 1), (1, 2), (2, 3)], [0, 1, 1, 2]),
+                   gi.clique(3), gi.cycle(4)]
+        # shared pool counter: rank 0 owns it, the others map it through CUDA IPC
+        if rank == 0:
+            ptr, handle = gm.gm_pool_counter_create()
+        else:
+            ptr, handle = None, None
+        box = [handle]
+        dist.broadcast_object_list(box, src=0)
+        if rank != 0:
+            ptr = gm.gm_pool_counter_open(box[0])
+        static = torch.zeros(len(queries), dtype=torch.int64)
+        shared = torch.zeros(len(queries), dtype=torch.int64)
+        for i, q in enumerate(queries):
+            p = gm.gm_plan_query(g, q)
+            static[i] = gm.gm_count(p, rank=rank, world=world, root_chunk=8, tau=64)[0]
+            if rank == 0:
+                gm.gm_pool_counter_reset(ptr)
+                torch.cuda.synchronize()
+            dist.barrier()
+            shared[i] = gm.gm_count(p, shared_pool_ctr=ptr, tau=256)[0]
+            dist.barrier()
+        dist.all_reduce(static)
+        dist.all_reduce(shared)
+        if rank == 0:
+            from oracle import OracleGraph
+            og = OracleGraph(n, s, d, lab)
+            single = [gm.gm_count(gm.gm_plan_query(g, q))[0] for q in queries]
+            ref = [og.count(q) for q in queries]
+            out.put((static.tolist(), shared.tolist(), single, ref))
+        dist.barrier()
+        gm.gm_pool_counter_close(ptr, owner=(rank == 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_static_and_shared_pool():
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    static, shared, single, ref = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert static == ref
+    assert shared == ref
+    assert single == ref
