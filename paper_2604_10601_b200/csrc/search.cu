@@ -97,6 +97,8 @@ struct SearchParams {
     uint32_t last_adj;          // positions adjacent to phi[last_b] in Q
     uint32_t last_low;          // deepest level prep_last must visit
     uint32_t last_k;            // popc(last_same & ~last_adj & below last-1): parked images per parent
+    uint32_t last_ka;           // with last_sb: popc(last_same & last_adj & below last-1), parked after
+    uint32_t last_sb;           // 1: phi[last] carries symmetry-breaking bounds
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
@@ -171,6 +173,8 @@ struct WarpStack {
     uint32_t chk[D][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
     uint32_t lastw[D][32];// set counting: per parent lane at level last-2, the same-label images to test
     uint32_t lastmb[32];  //               and the image of phi[last]'s backward neighbour (if < last-1)
+    uint32_t lastlb[32];  //               symmetry-breaking bounds of phi[last] from levels < last-1:
+    uint32_t lastub[32];  //               its image must lie in [lastlb, lastub)
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
 };
@@ -328,16 +332,23 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     if (!valid) return;
     const int b = (int)P.last_b;
     const uint32_t test = P.last_same & ~P.last_adj;
-    uint32_t mb = 0;
-    int k = 0;
+    const uint32_t known = P.last_sb ? (P.last_same & P.last_adj) : 0u;   // parked only with bounds
+    const uint32_t gt = P.sb_gt[l + 1], lt = P.sb_lt[l + 1];
+    uint32_t mb = 0, lb = 0, ub = 0xffffffffu;
+    int k = 0, ka = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.last_low; --i) {
         const uint32_t w = S.v[i][p];
         if (i == b) mb = w;
         if ((test >> i) & 1u) { S.lastw[k][lane] = w; ++k; }
+        if ((known >> i) & 1u) { S.lastw[P.last_k + ka][lane] = w; ++ka; }
+        if ((gt >> i) & 1u) lb = max(lb, w + 1);
+        if ((lt >> i) & 1u) ub = min(ub, w);
         p = S.pid[i][p];
     }
     S.lastmb[lane] = mb;
+    S.lastlb[lane] = lb;
+    S.lastub[lane] = ub;
 }
 
 template <int D>
@@ -349,6 +360,30 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     const uint32_t row = mb * P.S + lab;
     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
     words += 2;
+    if (P.last_sb) {
+        // symmetry breaking bounds phi[last]'s image to [lb, ub): count that part of the sorted
+        // slice, then remove the mapped same-label vertices inside it
+        uint32_t lb = S.lastlb[src], ub = S.lastub[src];
+        if ((P.sb_gt[l + 1] >> l) & 1u) lb = max(lb, v + 1);
+        if ((P.sb_lt[l + 1] >> l) & 1u) ub = min(ub, v);
+        if (lb >= ub) return 0;
+        const uint32_t len = hi - lo;
+        const uint32_t a = lb ? lower_bound_idx(P.nbr + lo, len, lb, words) : 0u;
+        const uint32_t e = ub != 0xffffffffu ? lower_bound_idx(P.nbr + lo, len, ub, words) : len;
+        uint32_t cnt = e > a ? e - a : 0u;
+        if (((same >> l) & 1u) && v >= lb && v < ub &&
+            (((P.last_adj >> l) & 1u) || has_edge(P, mb, lab, v, words)))
+            --cnt;
+        for (uint32_t c = 0; c < P.last_k; ++c) {
+            const uint32_t w = S.lastw[c][src];
+            if (w >= lb && w < ub && has_edge(P, mb, lab, w, words)) --cnt;
+        }
+        for (uint32_t c = 0; c < P.last_ka; ++c) {
+            const uint32_t w = S.lastw[P.last_k + c][src];
+            if (w >= lb && w < ub) --cnt;
+        }
+        return cnt;
+    }
     // mapped vertices adjacent to phi[b] in Q lie in the slice for sure (same label)
     uint32_t cnt = hi - lo - (uint32_t)__popc(same & P.last_adj & ((2u << l) - 1));
     if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lab, v, words)) --cnt;
@@ -930,15 +965,10 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     GM_CK(cudaEventRecord(e0, st));
 
     // symmetry breaking (count only): embeddings satisfying the plan's conditions, times |Aut(Q)|.
-    // Not when a condition would land on phi[last] while last-level set counting applies
-    // (one backward neighbour): set counting saves far more than the |Aut| factor there.
-    const bool set_count_ok = !enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && p->nq >= 2 &&
-                              __builtin_popcount(p->bw[p->nq - 1]) == 1;
-    // Also not with a user root list: "embeddings whose root is in the list" is not a union of
+    // Not with a user root list: "embeddings whose root is in the list" is not a union of
     // Aut(Q)-orbits.  (A rank partition is fine: every orbit representative has one root, so
     // the ranks' representative counts add up to the full one.)
-    const bool use_sb = !enumerate && p->sb_ok && p->aut > 1 && !(o.flags & GM_FLAG_NO_SYMMETRY) && !o.roots &&
-                        !(set_count_ok && (p->sb_gt[p->nq - 1] | p->sb_lt[p->nq - 1]));
+    const bool use_sb = !enumerate && p->sb_ok && p->aut > 1 && !(o.flags & GM_FLAG_NO_SYMMETRY) && !o.roots;
     rs.automorphisms = use_sb ? p->aut : 1;
 
     SearchParams P;
@@ -1115,9 +1145,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.limit_ns = o.time_limit_ms > 0 ? (unsigned long long)(o.time_limit_ms * 1e6) : 0ull;
         {   // last-level set counting applies when phi[last] has exactly one backward neighbour
             const uint32_t last = p->nq - 1, bwl = p->bw[last];
-            // (not when phi[last] carries symmetry-breaking bounds: those are checked per task)
-            if (!enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && last >= 1 && __builtin_popcount(bwl) == 1 &&
-                !(P.sb_gt[last] | P.sb_lt[last])) {
+            if (!enumerate && !(o.flags & GM_FLAG_NO_SET_COUNT) && last >= 1 && __builtin_popcount(bwl) == 1) {
                 const uint32_t b = (uint32_t)__builtin_ctz(bwl);
                 P.bulk_last = 1;
                 P.last_b = b;
@@ -1126,9 +1154,13 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                     if ((p->qadj[p->order[b]] >> p->order[i]) & 1u) P.last_adj |= 1u << i;
                 }
                 const uint32_t l = last - 1;   // the level count_last runs at
-                const uint32_t need = (b < l ? 1u << b : 0u) | (P.last_same & ~P.last_adj & ((1u << l) - 1));
+                const uint32_t below = (1u << l) - 1;
+                P.last_sb = (P.sb_gt[last] | P.sb_lt[last]) ? 1u : 0u;
+                uint32_t need = (b < l ? 1u << b : 0u) | (P.last_same & ~P.last_adj & below);
+                if (P.last_sb) need |= (P.last_same & P.last_adj & below) | ((P.sb_gt[last] | P.sb_lt[last]) & below);
                 P.last_low = need ? (uint32_t)__builtin_ctz(need) : l;
-                P.last_k = (uint32_t)__builtin_popcount(P.last_same & ~P.last_adj & ((1u << l) - 1));
+                P.last_k = (uint32_t)__builtin_popcount(P.last_same & ~P.last_adj & below);
+                P.last_ka = P.last_sb ? (uint32_t)__builtin_popcount(P.last_same & P.last_adj & below) : 0u;
             }
         }
         GM_CK(cudaEventRecord(d0e, st));
