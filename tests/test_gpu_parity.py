@@ -327,6 +327,68 @@ def test_config1_full(gm):
     assert total == len(ref) and np.array_equal(sorted_rows(rows), ref)
 
 
+def _device_graph(cfg):
+    import bench
+    n, s, d, lab = bench.make_graph_device(cfg)
+    return n, s, d, lab
+
+
+def test_config3_sampled_roots(gm):
+    """configs[2]: R-MAT scale 22 unlabelled (64M sampled edges), triangle / 4-clique / 5-cycle in
+    the bench configuration: per-root counts on sampled roots equal the oracle's; the full
+    triangle count with symmetry breaking equals the full search without it."""
+    import bench
+    cfg = bench.CONFIGS["rmat22"]
+    n, s, d, lab = _device_graph(cfg)
+    sh, dh = s.cpu().numpy().view(np.uint32), d.cpu().numpy().view(np.uint32)
+    g = gm.gm_load_graph(n, s, d, lab, 1)
+    og = OracleGraph(n, sh, dh)
+    rs = np.random.default_rng(3)
+    checked = nonzero = 0
+    for q in (gi.triangle(), gi.clique(4), gi.cycle(5)):
+        p = gm.gm_plan_query(g, q)
+        u0 = p.info()["order"][0]
+        roots, ref = [], 0
+        for v in rs.choice(n, 400, replace=False):
+            c = og.count(q, fixed=(u0, int(v)), max_nodes=200_000)
+            if c is not None:
+                roots.append(int(v)); ref += c; nonzero += c > 0
+            if len(roots) == 12:
+                break
+        assert gm.gm_count(p, roots=np.array(roots, np.uint32))[0] == ref
+        checked += len(roots)
+    assert checked >= 24 and nonzero >= 6
+    p = gm.gm_plan_query(g, gi.triangle())
+    c_sb, st = gm.gm_count(p)
+    assert st["automorphisms"] == 6 and st["timed_out"] == 0
+    assert c_sb == gm.gm_count(p, symmetry=False)[0]
+
+
+def test_config4_enumerated_rows_valid(gm):
+    """configs[3]: R-MAT scale 24, 16 labels, the bench's 16-vertex dense queries: rows listed by
+    gm_enumerate (time-limited) are distinct embeddings -- labels, injectivity, and every query
+    edge checked against the device edge list by an independent scan (gminputs.gpu)."""
+    import bench
+    import gminputs.gpu as gg
+    cfg = bench.CONFIGS["rmat24"]
+    n, s, d, lab = _device_graph(cfg)
+    lh = lab.cpu().numpy().view(np.uint32)
+    adj = gg.DeviceNeighbors(n, s, d)
+    queries = bench.build_queries(cfg, adj, lh)[:2]
+    g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
+    for q in queries:
+        p = gm.gm_plan_query(g, q)
+        rows, total, st = gm.gm_enumerate(p, capacity=256, time_limit_ms=500)
+        assert len(rows) == min(256, total) and len(rows) > 0
+        assert len({tuple(r) for r in rows.tolist()}) == len(rows)
+        for r in rows[:6].astype(np.int64):
+            assert len(set(r.tolist())) == q.n and np.array_equal(lh[r], q.labels)
+            for a, b in q.edges.tolist():
+                nb = adj.neighbors(int(r[a]))
+                i = np.searchsorted(nb, r[b])
+                assert i < len(nb) and nb[i] == r[b]
+
+
 def test_config2_sampled_roots(gm):
     """configs[1]: R-MAT scale 18 (16 edges/vertex), 8 labels, 8-vertex queries (§6.1 generator):
     GPU count restricted to sampled roots == sum of the oracle's per-root counts.  Roots are
@@ -442,7 +504,7 @@ def _aut_brute(q):
                and all((pm[a], pm[b]) in E for a, b in E))
 
 
-SYM_QUERIES = [gi.triangle(), gi.clique(4), gi.clique(5), gi.cycle(4), gi.cycle(5), gi.cycle(6), gi.star(3),
+SYM_QUERIES = [gi.path(2), gi.triangle(), gi.clique(4), gi.clique(5), gi.cycle(4), gi.cycle(5), gi.cycle(6), gi.star(3),
                gi.path(4), gi.Query(3, [(0, 1), (1, 2), (0, 2)], [0, 0, 1]),
                gi.Query(4, [(0, 1), (1, 2), (2, 3), (3, 0)], [0, 1, 0, 1]),
                gi.Query(5, [(0, 1), (0, 2), (0, 3), (0, 4), (1, 2)], [0, 1, 1, 2, 2])]
