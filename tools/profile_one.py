@@ -25,6 +25,8 @@ else:
     adj = None                      # fixed patterns only
 qs = bench.build_queries(cfg, adj, lh)
 g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
+if os.environ.get("GM_HUB_MB"):                 # hub-index sweeps
+    g.build_hubs(int(float(os.environ["GM_HUB_MB"]) * (1 << 20)), int(os.environ.get("GM_HUB_MIN", "64")))
 q = qs[qi]
 p = gm.gm_plan_query(g, q)
 u0 = p.info()["order"][0]
@@ -32,7 +34,8 @@ cands = np.flatnonzero(p.candidates(u0))
 roots = np.random.default_rng(0).permutation(cands)[:nroots].astype(np.uint32) if nroots > 0 else None
 for it in range(2):
     t = time.time()
-    c, st = gm.gm_count(p, roots=roots, tau=tau, time_limit_ms=float(os.environ.get("GM_LIMIT_MS", "0")))
+    c, st = gm.gm_count(p, roots=roots, tau=tau, time_limit_ms=float(os.environ.get("GM_LIMIT_MS", "0")),
+                        warps_per_block=int(os.environ.get("GM_WPB", "0")))
     print(q.name, len(q.edges), c, f"wall {time.time() - t:.3f}s",
           {k: st[k] for k in ("dfs_ms", "total_ms", "tasks", "words", "pool_size", "pool_depth", "donations",
                               "grid", "block")}, flush=True)
