@@ -959,7 +959,17 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     memset(&rs, 0, sizeof(rs));
     uint32_t launches = 0;
 
-    cudaEvent_t e0, e1, d0e, d1e;
+    // every early return (GM_CK / GM_REQ) releases what this call created
+    cudaEvent_t e0 = nullptr, e1 = nullptr, d0e = nullptr, d1e = nullptr;
+    uint32_t *d_user = nullptr, *enum_dev = nullptr;
+    struct Release {
+        cudaEvent_t *ev[4];
+        uint32_t **buf[2];
+        ~Release() {
+            for (auto e : ev) if (*e) cudaEventDestroy(*e);
+            for (auto b : buf) if (*b) cudaFree(*b);
+        }
+    } release{{&e0, &e1, &d0e, &d1e}, {&d_user, &enum_dev}};
     GM_CK(cudaEventCreate(&e0)); GM_CK(cudaEventCreate(&e1));
     GM_CK(cudaEventCreate(&d0e)); GM_CK(cudaEventCreate(&d1e));
     GM_CK(cudaEventRecord(e0, st));
@@ -1004,7 +1014,6 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     unsigned long long *ctr_aux = &W.ctrl->out_ctr;
 
     // ---- root candidates (rank share)
-    uint32_t *d_user = nullptr;
     // a non-NULL root list restricts phi[0]'s images to it (an empty list: no embeddings)
     const unsigned long long nroot_cap = o.roots ? o.num_roots : g->n;
     int rc = ensure(W.buf[0], W.buf_bytes[0], sizeof(uint32_t) * (nroot_cap ? nroot_cap : 1));
@@ -1032,7 +1041,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     unsigned long long nroots = 0;
     GM_CK(cudaMemcpyAsync(&nroots, ctr_aux, sizeof(nroots), cudaMemcpyDeviceToHost, st));
     GM_CK(cudaStreamSynchronize(st));
-    if (d_user) cudaFree(d_user);
+    if (d_user) { cudaFree(d_user); d_user = nullptr; }
     rs.roots = nroots;
 
     uint32_t *frontier = W.buf[0];
@@ -1059,12 +1068,16 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         }
         done = true;
     }
-    uint32_t *enum_dev = nullptr;   // device staging for host-side enumerate output
-    auto out_dev = [&]() -> uint32_t * {
-        if (mem == GM_MEM_DEVICE) return out;
-        if (!enum_dev && cap) cudaMalloc(&enum_dev, sizeof(uint32_t) * cap * p->nq);
-        return enum_dev;
-    };
+    // enum_dev: device staging for host-side enumerate output (released by `release`)
+    if (enumerate && mem != GM_MEM_DEVICE && cap) {
+        if (cudaMalloc(&enum_dev, sizeof(uint32_t) * cap * p->nq) != cudaSuccess) {
+            cudaGetLastError();
+            enum_dev = nullptr;
+            set_error("gm_enumerate: cannot stage %llu rows on the device", (unsigned long long)cap);
+            return GM_ERR_NOMEM;
+        }
+    }
+    auto out_dev = [&]() -> uint32_t * { return mem == GM_MEM_DEVICE ? out : enum_dev; };
 
     // ---- initialization phase: BFS to tau partial matches (§4.3)
     while (!done) {
@@ -1203,9 +1216,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     }
     GM_CK(cudaEventRecord(e1, st));
     GM_CK(cudaStreamSynchronize(st));
-    if (enum_dev) cudaFree(enum_dev);
     GM_CK(cudaEventElapsedTime(&rs.total_ms, e0, e1));
-    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(d0e); cudaEventDestroy(d1e);
     rs.count = total;
     rs.kernel_launches = launches;
     if (stats) *stats = rs;
