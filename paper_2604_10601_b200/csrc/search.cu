@@ -1052,23 +1052,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     bool done = false;
     unsigned long long zero = 0;
 
-    if (p->nq == 1) {
-        total = nroots;
-        if (enumerate && nroots) {
-            uint32_t *dst = out;
-            uint32_t *tmp = nullptr;
-            if (mem == GM_MEM_HOST) { GM_CK(cudaMalloc(&tmp, sizeof(uint32_t) * std::max<uint64_t>(1, std::min<uint64_t>(cap, nroots)))); dst = tmp; }
-            k_write_single<<<grid_for(nroots, 256, W.sms), 256, 0, st>>>(frontier, nroots, dst, cap, g->new2old);
-            ++launches;
-            if (tmp) {
-                GM_CK(cudaMemcpyAsync(out, tmp, sizeof(uint32_t) * std::min<uint64_t>(cap, nroots), cudaMemcpyDeviceToHost, st));
-                GM_CK(cudaStreamSynchronize(st));
-                cudaFree(tmp);
-            }
-        }
-        done = true;
-    }
-    // enum_dev: device staging for host-side enumerate output (released by `release`)
+    // enum_dev: device staging for host-side enumerate output (released by `release`;
+    // copied to `out` once, at the end)
     if (enumerate && mem != GM_MEM_DEVICE && cap) {
         if (cudaMalloc(&enum_dev, sizeof(uint32_t) * cap * p->nq) != cudaSuccess) {
             cudaGetLastError();
@@ -1078,6 +1063,16 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         }
     }
     auto out_dev = [&]() -> uint32_t * { return mem == GM_MEM_DEVICE ? out : enum_dev; };
+
+    if (p->nq == 1) {
+        total = nroots;
+        if (enumerate && nroots && cap) {
+            k_write_single<<<grid_for(nroots, 256, W.sms), 256, 0, st>>>(frontier, nroots, out_dev(), cap, g->new2old);
+            GM_CK(cudaGetLastError());
+            ++launches;
+        }
+        done = true;
+    }
 
     // ---- initialization phase: BFS to tau partial matches (§4.3)
     while (!done) {
