@@ -103,6 +103,33 @@ class DeviceNeighbors:
         self.cache[v] = nb
         return nb
 
+    def induced_edges(self, vs):
+        """Edges of the simple graph with both endpoints in vs, as a sorted (k, 2) array of
+        (a, b) pairs with a < b (one edge scan)."""
+        import torch
+        self.bits.zero_()
+        bits = np.zeros(self.bits.numel(), np.uint32)
+        for v in vs:
+            bits[v >> 5] |= np.uint32(1 << (v & 31))
+        self.bits.copy_(torch.from_numpy(bits.view(np.int32)))
+        cap = 1 << 22
+        while True:
+            self.cnt.zero_()
+            os_ = torch.empty(cap, dtype=torch.int32, device=self.src.device)
+            od = torch.empty(cap, dtype=torch.int32, device=self.src.device)
+            assert _load().gen_incident(self.src.numel(), self.src.data_ptr(), self.dst.data_ptr(),
+                                        self.bits.data_ptr(), os_.data_ptr(), od.data_ptr(), self.cnt.data_ptr(),
+                                        cap, _stream()) == 0
+            k = int(self.cnt.item())
+            if k <= cap:
+                break
+            cap = 1 << int(np.ceil(np.log2(k)))
+        s = os_[:k].cpu().numpy().view(np.uint32)
+        d = od[:k].cpu().numpy().view(np.uint32)
+        keep = np.isin(s, np.asarray(vs, np.uint32)) & np.isin(d, np.asarray(vs, np.uint32)) & (s != d)
+        a, b = np.minimum(s[keep], d[keep]), np.maximum(s[keep], d[keep])
+        return np.unique(np.stack([a, b], 1), axis=0) if len(a) else np.zeros((0, 2), np.uint32)
+
     def of_set(self, vs):
         """{v: sorted neighbour array} for every v in vs (one edge scan)."""
         import torch

@@ -42,6 +42,9 @@
 namespace gm {
 
 constexpr uint32_t FULL = 0xffffffffu;
+#ifndef GM_DFS_MINB
+#define GM_DFS_MINB 9
+#endif
 constexpr uint32_t kItemWords = 4 + kMaxQ;     // [depth, cb, cl, cs, prefix[kMaxQ]]
 
 // Global control block.  Every field that many warps poll or update lives on its own
@@ -170,8 +173,14 @@ struct WarpStack {
     uint32_t cl[D][32];   //                  its length
     uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
     uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
-    uint32_t chk[D][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
-    uint32_t lastw[D][32];// set counting: per parent lane at level last-2, the same-label images to test
+#ifndef GM_CHK_ROWS
+#define GM_CHK_ROWS D
+#endif
+#ifndef GM_LASTW_ROWS
+#define GM_LASTW_ROWS D
+#endif
+    uint32_t chk[GM_CHK_ROWS][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
+    uint32_t lastw[GM_LASTW_ROWS][32];// set counting: per parent lane at level last-2, the same-label images to test
     uint32_t lastmb[32];  //               and the image of phi[last]'s backward neighbour (if < last-1)
     uint32_t lastlb[32];  //               symmetry-breaking bounds of phi[last] from levels < last-1:
     uint32_t lastub[32];  //               its image must lie in [lastlb, lastub)
@@ -405,7 +414,7 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // ------------------------------------------------------------------ DFS kernel
 
 template <int D, bool ENUM>
-__global__ void __launch_bounds__(128, 9) k_dfs(const SearchParams P) {
+__global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     WarpStack<D> &S = reinterpret_cast<WarpStack<D> *>(smem_raw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;

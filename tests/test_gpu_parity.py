@@ -531,3 +531,61 @@ def test_symmetry_breaking_counts(gm, qi):
             assert c == ref and st["automorphisms"] in (1, info["automorphisms"])
             assert gm.gm_count(p, tau=tau, symmetry=False)[0] == ref
             assert gm.gm_count(p, tau=tau, set_count=False)[0] == ref
+
+
+def test_config5_local_parity(gm):
+    """configs[4]: Friendster-shaped R-MAT scale 26 (2.1 G adjacency entries, 16 labels) with the
+    bench's 24/32-vertex dense queries.  (a) Exact parity at full size: for the sub-query induced
+    by a query vertex c and up to 4 of its Q-neighbours, every embedding with M[c] = v lies in
+    the closed neighbourhood N[v]; the oracle counts it on that local graph (edges gathered by
+    an independent scan of the device edge list) and the GPU counts it on the whole graph with
+    root v.  (b) Rows listed by gm_enumerate for the full queries are distinct embeddings."""
+    import bench
+    import gminputs.gpu as gg
+    cfg = bench.CONFIGS["rmat26"]
+    n, s, d, lab = _device_graph(cfg)
+    lh = lab.cpu().numpy().view(np.uint32)
+    adj = gg.DeviceNeighbors(n, s, d)
+    queries = bench.build_queries(cfg, adj, lh)
+    queries = [queries[0], queries[2]]                       # one 24- and one 32-vertex query
+    g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
+    rs = np.random.default_rng(26)
+    checked = nonzero = 0
+    for q in queries:
+        qe = q.edges.tolist()
+        qn = {u: sorted({b for a, b in qe if a == u} | {a for a, b in qe if b == u}) for u in range(q.n)}
+        c = max(range(q.n), key=lambda u: (len(qn[u]), -u))
+        for k in (2, 4):
+            keep = [c] + qn[c][:k]
+            idx = {u: i for i, u in enumerate(keep)}
+            sub = gi.Query(len(keep), [(idx[a], idx[b]) for a, b in qe if a in idx and b in idx],
+                           [int(q.labels[u]) for u in keep])
+            ps = gm.gm_plan_query(g, sub, order=list(range(len(keep))))
+            cands = np.flatnonzero(ps.candidates(0))
+            roots, ref = [], 0
+            for v in rs.permutation(cands)[:200]:
+                nv = adj.neighbors(int(v))
+                if not 2 <= len(nv) <= 160:
+                    continue
+                ball = [int(v)] + nv.tolist()
+                loc = {w: i for i, w in enumerate(ball)}
+                es = np.array([(loc[a], loc[b]) for a, b in adj.induced_edges(ball).tolist()], np.uint32).reshape(-1, 2)
+                og = OracleGraph(len(ball), es[:, 0].copy(), es[:, 1].copy(), lh[np.array(ball, np.int64)])
+                cnt = og.count(sub, fixed=(0, 0))
+                roots.append(int(v)); ref += cnt; nonzero += cnt > 0
+                assert gm.gm_count(ps, roots=np.array([v], np.uint32))[0] == cnt, (q.name, k, int(v))
+                if len(roots) == 4:
+                    break
+            assert gm.gm_count(ps, roots=np.array(roots, np.uint32))[0] == ref
+            checked += len(roots)
+        p = gm.gm_plan_query(g, q)
+        rows, total, st = gm.gm_enumerate(p, capacity=128, time_limit_ms=500)
+        assert len(rows) == min(128, total) and len(rows) > 0
+        assert len({tuple(r) for r in rows.tolist()}) == len(rows)
+        for r in rows[:4].astype(np.int64):
+            assert len(set(r.tolist())) == q.n and np.array_equal(lh[r], q.labels)
+            for a, b in qe:
+                nb = adj.neighbors(int(r[a]))
+                i = np.searchsorted(nb, r[b])
+                assert i < len(nb) and nb[i] == r[b]
+    assert checked >= 12 and nonzero >= 3
