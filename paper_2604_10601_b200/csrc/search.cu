@@ -42,6 +42,9 @@
 namespace gm {
 
 constexpr uint32_t FULL = 0xffffffffu;
+#ifndef GM_VHUB
+#define GM_VHUB 1
+#endif
 #ifndef GM_DFS_MINB
 #define GM_DFS_MINB 9
 #endif
@@ -147,17 +150,21 @@ __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint
     return (ld_nc(P.cand + P.candoff[l] + (v >> 5)) >> (v & 31)) & 1u;
 }
 
-// v in N_lab(w)?  (v is known to have label lab.)  Hub bitmap if w is a hub (w < nhubs:
-// device ids are ordered by degree), else a binary search of w's label-lab row.
-__device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t w, uint32_t lab, uint32_t v,
+// Is {a, b} an edge?  la = L(a), lb = L(b).  The test is symmetric (b in N_lb(a) iff a in
+// N_la(b)), so it takes the cheapest side: the hub bitmap of a or of b if either is a hub
+// (device ids are ordered by degree: "is a hub" is w < nhubs), else a binary search of the
+// row of the LOWER-degree vertex (the larger device id), which is the shorter list.
+__device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t a, uint32_t la, uint32_t b, uint32_t lb,
                                          uint32_t &words) {
-    if (w < P.nhubs) {
+    if (a < P.nhubs || b < P.nhubs) {
+        const uint32_t h = a < P.nhubs ? a : b, x = a < P.nhubs ? b : a;
         ++words;
-        return (ld_nc(P.hub_bits + (unsigned long long)w * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+        return (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
     }
-    const uint32_t row = w * P.S + lab;
+    const uint32_t r = a > b ? a : b, x = a > b ? b : a, lx = a > b ? lb : la;
+    const uint32_t row = r * P.S + lx;
     words += 2;
-    return contains(P.nbr, ld_nc(P.offs + row), ld_nc(P.offs + row + 1), v, words);
+    return contains(P.nbr, ld_nc(P.offs + row), ld_nc(P.offs + row + 1), x, words);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -174,10 +181,10 @@ struct WarpStack {
     uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
     uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
 #ifndef GM_CHK_ROWS
-#define GM_CHK_ROWS D
+#define GM_CHK_ROWS (D - 2)   // checks per task <= |bw| - 1 <= D - 2
 #endif
 #ifndef GM_LASTW_ROWS
-#define GM_LASTW_ROWS D
+#define GM_LASTW_ROWS (D - 2) // set-counting images: positions < last - 1
 #endif
     uint32_t chk[GM_CHK_ROWS][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
     uint32_t lastw[GM_LASTW_ROWS][32];// set counting: per parent lane at level last-2, the same-label images to test
@@ -280,8 +287,10 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         bool r0 = true, r1 = true, need0 = false, need1 = false;
         uint32_t b0 = 0, n0 = 0, b1 = 0, n1 = 0;
         if (ok) {
-            if (w0 < P.nhubs) {
-                r0 = (ld_nc(P.hub_bits + (unsigned long long)w0 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+            // hub bitmap of w, or of v (the test is symmetric), else binary search of w's row
+            if (w0 < P.nhubs || (GM_VHUB && v < P.nhubs)) {
+                const uint32_t h = w0 < P.nhubs ? w0 : v, x = w0 < P.nhubs ? v : w0;
+                r0 = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
                 ++words;
             } else {
                 const uint32_t row = w0 * P.S + lab;
@@ -291,8 +300,9 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
                 words += 2;
             }
             if (two) {
-                if (w1 < P.nhubs) {
-                    r1 = (ld_nc(P.hub_bits + (unsigned long long)w1 * P.hub_words + (v >> 5)) >> (v & 31)) & 1u;
+                if (w1 < P.nhubs || (GM_VHUB && v < P.nhubs)) {
+                    const uint32_t h = w1 < P.nhubs ? w1 : v, x = w1 < P.nhubs ? v : w1;
+                    r1 = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
                     ++words;
                 } else {
                     const uint32_t row = w1 * P.S + lab;
@@ -366,6 +376,7 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     const uint32_t lab = P.lab[l + 1];
     const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
     const uint32_t mb = (int)P.last_b == l ? v : S.lastmb[src];   // M[b]
+    const uint32_t lb_lab = P.lab[P.last_b];                       // L(M[b])
     const uint32_t row = mb * P.S + lab;
     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
     words += 2;
@@ -381,11 +392,11 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
         const uint32_t e = ub != 0xffffffffu ? lower_bound_idx(P.nbr + lo, len, ub, words) : len;
         uint32_t cnt = e > a ? e - a : 0u;
         if (((same >> l) & 1u) && v >= lb && v < ub &&
-            (((P.last_adj >> l) & 1u) || has_edge(P, mb, lab, v, words)))
+            (((P.last_adj >> l) & 1u) || has_edge(P, mb, lb_lab, v, lab, words)))
             --cnt;
         for (uint32_t c = 0; c < P.last_k; ++c) {
             const uint32_t w = S.lastw[c][src];
-            if (w >= lb && w < ub && has_edge(P, mb, lab, w, words)) --cnt;
+            if (w >= lb && w < ub && has_edge(P, mb, lb_lab, w, lab, words)) --cnt;
         }
         for (uint32_t c = 0; c < P.last_ka; ++c) {
             const uint32_t w = S.lastw[P.last_k + c][src];
@@ -395,9 +406,9 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     }
     // mapped vertices adjacent to phi[b] in Q lie in the slice for sure (same label)
     uint32_t cnt = hi - lo - (uint32_t)__popc(same & P.last_adj & ((2u << l) - 1));
-    if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lab, v, words)) --cnt;
+    if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lb_lab, v, lab, words)) --cnt;
     for (uint32_t c = 0; c < P.last_k; ++c)
-        if (has_edge(P, mb, lab, S.lastw[c][src], words)) --cnt;
+        if (has_edge(P, mb, lb_lab, S.lastw[c][src], lab, words)) --cnt;
     return cnt;
 }
 
@@ -765,7 +776,7 @@ __global__ void __launch_bounds__(256) k_expand(const SearchParams P, const uint
                 if (F && v == mi) F = false;
                 if (F && ((gt >> i) & 1u) && !(v > mi)) F = false;      // symmetry breaking
                 if (F && ((lt >> i) & 1u) && !(v < mi)) F = false;
-                if (F && ((checks >> i) & 1u)) F = has_edge(P, mi, lab, v, scratch);
+                if (F && ((checks >> i) & 1u)) F = has_edge(P, mi, P.lab[i], v, lab, scratch);
             }
             const uint32_t fm = __ballot_sync(FULL, F);
             if (MODE == 0) {
