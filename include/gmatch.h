@@ -98,8 +98,10 @@ GM_API int gm_graph_info(const gm_graph *g, gm_graph_info_t *info);
  * gm_graph_build_hubs -- (re)build the hub adjacency index: for the highest-degree
  * vertices (degree >= min_degree, at most budget_bytes / (4*ceil(n/32)) of them) a bitmap
  * of N(v) over all vertex ids, used by the search to test v in N(w) with one word read
- * instead of a binary search.  gm_load_graph builds it with a
- * 64 MiB budget and min_degree 64; budget_bytes = 0 removes it.  Results never depend on it.
+ * instead of a binary search.  gm_load_graph builds it with
+ * min_degree 64 and a 64 MiB budget when the CSR fits in L2 beside it, else an 8 GiB budget
+ * (at most a quarter of the free device memory); budget_bytes = 0 removes it.  Results
+ * never depend on it.
  * Synchronizes `stream`.  Do not call while a search on this graph is running.
  */
 GM_API int gm_graph_build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, void *stream);
@@ -215,7 +217,8 @@ typedef struct {
  *   count_out   one uint64 in `mem` receiving the count (device memory lets the
  *               caller all-reduce it across ranks without a host round trip).
  *   stats       optional host struct.
- * Returns GM_OK, or GM_TIMEOUT (count is the number found before the limit).
+ * Returns GM_OK, or GM_TIMEOUT (count is the number found before the limit), or
+ * GM_ERR_LIMIT when the count does not fit in 64 bits (count_out = UINT64_MAX).
  */
 GM_API int gm_count(const gm_plan *p, const gm_run_opts *opts, uint64_t *count_out, int mem,
              gm_run_stats *stats, void *stream);

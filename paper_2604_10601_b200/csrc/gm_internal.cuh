@@ -61,6 +61,10 @@ namespace gm {
 int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, cudaStream_t st);
 void free_hubs(gm_graph *g);
 constexpr uint64_t kDefaultHubBudget = 64ull << 20;   // fits beside the graph in the 126 MB L2
+constexpr uint64_t kLargeHubBudget = 8ull << 30;     // graphs whose CSR cannot stay in L2
+// default hub budget for a graph: the L2-resident budget when the CSR fits in L2 beside it,
+// else the large one (at most a quarter of the free device memory)
+uint64_t default_hub_budget(const gm_graph *g);
 constexpr uint32_t kDefaultHubMinDegree = 64;
 }  // namespace gm
 

@@ -28,6 +28,21 @@ __global__ void k_hub_bits(uint32_t S, const uint32_t *__restrict__ offs, const 
     }
 }
 
+uint64_t default_hub_budget(const gm_graph *g) {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const uint64_t csr = 4ull * (g->n * g->S + 1 + g->nadj);
+    // measured: on rmat18 (30 MB CSR) the 64 MiB index stays in L2 beside the
+    // graph; on rmat24/26 every probe goes to DRAM anyway, and an 8 GiB index (one DRAM
+    // word per test against a hub instead of a dependent binary search) doubled tasks/s
+    if (csr + kDefaultHubBudget <= (uint64_t)l2) return kDefaultHubBudget;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return kDefaultHubBudget; }
+    const uint64_t cap = fr / 4;
+    return cap < kLargeHubBudget ? (cap > kDefaultHubBudget ? cap : kDefaultHubBudget) : kLargeHubBudget;
+}
+
 void free_hubs(gm_graph *g) {
     cudaFree(g->hub_bits);
     g->hub_bits = nullptr;

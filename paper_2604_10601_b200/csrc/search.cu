@@ -62,6 +62,7 @@ struct Ctrl {
     unsigned long long t0;                    // globaltimer at the first warp's start
     alignas(128) unsigned long long out_ctr;
     alignas(128) unsigned long long count;
+    int overflow;               // the count wrapped past 2^64 - 1
     unsigned long long tasks;
     unsigned long long rounds;
     unsigned long long words;   // algorithmic 4-byte words read by k_dfs
@@ -698,7 +699,10 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
         my_words += __shfl_xor_sync(FULL, my_words, o);
     }
     if (lane == 0) {
-        if (my_count) atomicAdd(&C->count, my_count);
+        if (my_count) {
+            const unsigned long long old = atomicAdd(&C->count, my_count);
+            if (old + my_count < old) atomicExch(&C->overflow, 1);
+        }
         atomicAdd(&C->tasks, my_tasks);
         atomicAdd(&C->words, my_words);
         atomicAdd(&C->rounds, my_rounds);
@@ -1069,7 +1073,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     unsigned long long P_n = nroots;
     uint32_t d = 1;
     unsigned long long total = 0;
-    bool done = false;
+    bool done = false, overflow = false;
     unsigned long long zero = 0;
 
     // enum_dev: device staging for host-side enumerate output (released by `release`;
@@ -1210,6 +1214,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         GM_CK(cudaMemcpyAsync(&h, W.ctrl, sizeof(h), cudaMemcpyDeviceToHost, st));
         GM_CK(cudaStreamSynchronize(st));
         total = h.count;
+        overflow = h.overflow != 0;
         rs.tasks = h.tasks;
         rs.words = h.words;
         rs.rounds = h.rounds;
@@ -1217,7 +1222,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         rs.timed_out = h.abort ? 1 : 0;
         GM_CK(cudaEventElapsedTime(&rs.dfs_ms, d0e, d1e));
     }
-    if (use_sb) total *= p->aut;   // one embedding per Aut(Q)-orbit was counted
+    if (use_sb && __builtin_mul_overflow(total, (unsigned long long)p->aut, &total))   // one per Aut(Q)-orbit
+        overflow = true;
+    if (overflow) total = ~0ull;
     // ---- outputs
     if (enumerate && mem == GM_MEM_HOST && enum_dev && cap) {
         const uint64_t rows = std::min<uint64_t>(cap, total);
@@ -1235,6 +1242,10 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     rs.count = total;
     rs.kernel_launches = launches;
     if (stats) *stats = rs;
+    if (overflow) {
+        set_error("gm_count: the number of embeddings exceeds 2^64 - 1");
+        return GM_ERR_LIMIT;
+    }
     return rs.timed_out ? GM_TIMEOUT : GM_OK;
 }
 
