@@ -164,6 +164,9 @@ GM_API void gm_free_plan(gm_plan *p);
 #define GM_FLAG_NO_SET_COUNT 1u  /* gm_count: validate every last-level candidate as its own task
                                     (Alg. 2 as written) instead of set-counting the last level
                                     when phi[last] has a single backward neighbour */
+#define GM_FLAG_NO_PAIR_COUNT 4u /* gm_count: do not count the last two levels in bulk when
+                                    phi[last-1] and phi[last] are non-adjacent vertices with one
+                                    backward neighbour each (pair counting) */
 #define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
                                     Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)|.
                                     Symmetry breaking is also skipped when `roots` is given. */

@@ -177,7 +177,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
-          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True,
+          time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True, pair_count=True,
           shared_pool_ctr=None):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
@@ -202,6 +202,8 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.pool_bytes_max = int(pool_bytes_max)
     if not set_count:
         o.flags |= L.GM_FLAG_NO_SET_COUNT
+    if not pair_count:
+        o.flags |= L.GM_FLAG_NO_PAIR_COUNT
     if not symmetry:
         o.flags |= L.GM_FLAG_NO_SYMMETRY
     if shared_pool_ctr is not None:

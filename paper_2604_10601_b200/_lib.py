@@ -20,6 +20,7 @@ GM_MEM_HOST, GM_MEM_DEVICE = 0, 1
 GM_MAX_QUERY = 32
 GM_FLAG_NO_SET_COUNT = 1
 GM_FLAG_NO_SYMMETRY = 2
+GM_FLAG_NO_PAIR_COUNT = 4
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 
 # every symbol include/gmatch.h declares (checked by tests/test_abi.py)

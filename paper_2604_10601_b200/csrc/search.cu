@@ -69,6 +69,10 @@ struct Ctrl {
     unsigned long long donations;
 };
 
+#ifdef GM_LEVEL_STATS
+__device__ unsigned long long g_level_tasks[32], g_level_pass[32];   // debug build: tasks / passes per level
+#endif
+
 struct SearchParams {
     const uint32_t *__restrict__ offs;
     const uint32_t *__restrict__ nbr;
@@ -106,6 +110,11 @@ struct SearchParams {
     uint32_t last_k;            // popc(last_same & ~last_adj & below last-1): parked images per parent
     uint32_t last_ka;           // with last_sb: popc(last_same & last_adj & below last-1), parked after
     uint32_t last_sb;           // 1: phi[last] carries symmetry-breaking bounds
+    uint32_t bulk_two;          // 1: count the last TWO levels per partial match (count_two)
+    uint32_t two_b6, two_b7;    // positions of the single backward neighbours of phi[last-1], phi[last]
+    uint32_t two_same6, two_same7;  // positions i <= last-2 (i != b) labelled like phi[last-1] / phi[last]
+    uint32_t two_adj6, two_adj7;    // ... whose query vertex is adjacent to phi[b6] / phi[b7]
+    uint32_t two_low;           // deepest level count_two's walk visits
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
@@ -192,6 +201,7 @@ struct WarpStack {
     uint32_t lastmb[32];  //               and the image of phi[last]'s backward neighbour (if < last-1)
     uint32_t lastlb[32];  //               symmetry-breaking bounds of phi[last] from levels < last-1:
     uint32_t lastub[32];  //               its image must lie in [lastlb, lastub)
+    uint32_t tacc[32];    // pair counting: per-lane |A n R| accumulators
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
 };
@@ -411,6 +421,113 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     for (uint32_t c = 0; c < P.last_k; ++c)
         if (has_edge(P, mb, lb_lab, S.lastw[c][src], lab, words)) --cnt;
     return cnt;
+}
+
+// Pair counting (count mode): when phi[last-1] and phi[last] each
+// have ONE backward neighbour, b6 and b7, and are not adjacent to each other, the embeddings
+// extending a partial match M of depth last-1 (levels 0..l, l = last-2) are the pairs
+// (x, y) with x in A = N_{L(phi[last-1])}(M[b6]), y in R = N_{L(phi[last])}(M[b7]), neither
+// mapped in M, and x != y.  (Adjacency to the single backward neighbour is the only edge
+// constraint on each; both candidate filters are implied, as for count_last.)  With
+// V = A \ M and B = |R \ M|:
+//     count = |V| * B - [L(phi[last-1]) == L(phi[last])] * |V n R|,
+//     |V n R| = |A n R| - |M n A n R|,
+// where |A n R| (b6 != b7) is one sorted-list intersection, computed by the whole warp
+// (shorter list split over the lanes, each element tested against the longer list's hub
+// bitmap or by binary search).  Warp-collective: every lane calls it; F = lane has a valid
+// partial match ending in (l, v, src).
+template <int D>
+__device__ __forceinline__ unsigned long long count_two(const SearchParams &P, WarpStack<D> &S, int l,
+                                                        uint32_t v, uint32_t src, bool F, uint32_t lane,
+                                                        uint32_t &words) {
+    const uint32_t lab6 = P.lab[l + 1], lab7 = P.lab[l + 2];
+    const int b6 = (int)P.two_b6, b7 = (int)P.two_b7;
+    uint32_t m6 = v, m7 = v, a0 = 0, a1 = 0, r0 = 0, r1 = 0, inA = 0, inR = 0, inAR = 0;
+    if (F) {
+        uint32_t p = src;
+        for (int i = l - 1; i >= (int)P.two_low; --i) {   // M[b6], M[b7]
+            const uint32_t w = S.v[i][p];
+            if (i == b6) m6 = w;
+            if (i == b7) m7 = w;
+            p = S.pid[i][p];
+        }
+        const uint32_t ra = m6 * P.S + lab6, rr = m7 * P.S + lab7;
+        a0 = ld_nc(P.offs + ra); a1 = ld_nc(P.offs + ra + 1);
+        r0 = ld_nc(P.offs + rr); r1 = ld_nc(P.offs + rr + 1);
+        words += 4;
+        // mapped vertices inside A and R: only same-label ones can be; surely if their query
+        // vertex is adjacent to phi[b] in Q, else one edge test
+        p = src;
+        for (int i = l; i >= (int)P.two_low; --i) {
+            const uint32_t w = i == l ? v : S.v[i][p];
+            bool a = false, r = false;
+            if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge(P, m6, P.lab[b6], w, lab6, words);
+            if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge(P, m7, P.lab[b7], w, lab7, words);
+            inA += a; inR += r; inAR += a && r;
+            if (i < l) p = S.pid[i][p];
+        }
+    }
+    const unsigned long long nV = (unsigned long long)(a1 - a0 - inA), nB = (unsigned long long)(r1 - r0 - inR);
+    unsigned long long cnt = nV * nB;
+    if (lab6 == lab7) {                       // uniform
+        unsigned long long ar = 0;
+        if (b6 == b7) {
+            ar = a1 - a0;                     // A == R
+        } else {
+            // segmented intersection: the shorter lists of all lanes form one virtual pool of
+            // elements, dealt 32 per round like ScatterTask; each element is tested against its
+            // owner's longer list (hub bitmap, else binary search); hits are summed per owner
+            const bool a_short = a1 - a0 <= r1 - r0;
+            const uint32_t sb = a_short ? a0 : r0, sl = F ? (a_short ? a1 - a0 : r1 - r0) : 0u;
+            const uint32_t gb = a_short ? r0 : a0, ge = a_short ? r1 : a1, gown = a_short ? m7 : m6;
+            S.tacc[lane] = 0;
+            __syncwarp();
+            uint32_t ci = 0, cj = 0;
+            while (true) {
+                uint32_t rem = lane >= ci ? sl - (lane == ci ? cj : 0u) : 0u;
+                const uint32_t r32 = min(rem, 32u);
+                uint32_t incl = r32;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t x = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= (uint32_t)o) incl += x;
+                }
+                const uint32_t total = __shfl_sync(FULL, incl, 31);
+                if (total == 0) break;
+                const uint32_t k = min(total, 32u);
+                uint32_t src = 0;
+#pragma unroll
+                for (uint32_t bb = 16; bb >= 1; bb >>= 1) {
+                    const uint32_t x = __shfl_sync(FULL, incl, src + bb - 1);
+                    if (x <= lane) src += bb;
+                }
+                src = min(src, 31u);
+                const uint32_t src_excl = __shfl_sync(FULL, incl - r32, src);
+                const uint32_t off = lane < k ? lane - src_excl + (src == ci ? cj : 0u) : 0u;
+                const uint32_t s_sb = __shfl_sync(FULL, sb, src), s_gb = __shfl_sync(FULL, gb, src);
+                const uint32_t s_ge = __shfl_sync(FULL, ge, src), s_gown = __shfl_sync(FULL, gown, src);
+                const uint32_t lsrc = __shfl_sync(FULL, src, k - 1), loff = __shfl_sync(FULL, off, k - 1);
+                const uint32_t lsl = __shfl_sync(FULL, sl, lsrc);
+                if (loff + 1 < lsl) { ci = lsrc; cj = loff + 1; } else { ci = lsrc + 1; cj = 0; }
+                if (lane < k) {
+                    const uint32_t x = ld_nc(P.nbr + s_sb + off);
+                    ++words;
+                    bool hit;
+                    if (s_gown < P.nhubs) {
+                        ++words;
+                        hit = (ld_nc(P.hub_bits + (unsigned long long)s_gown * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+                    } else {
+                        hit = contains(P.nbr, s_gb, s_ge, x, words);
+                    }
+                    if (hit) atomicAdd(&S.tacc[src], 1u);
+                }
+            }
+            __syncwarp();
+            ar = S.tacc[lane];
+        }
+        if (F) cnt -= ar - inAR;
+    }
+    return F ? cnt : 0ull;
 }
 
 // Walk the chain of (level, lane) and write the prefix M[0..level] into dst (by position).
@@ -642,11 +759,24 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
             const uint32_t v = has ? ld_nc(P.nbr + S.cb[l][src] + off) : 0;
             my_rounds += (lane == 0);
             my_tasks += has;
+#ifdef GM_LEVEL_STATS
+            if (lane == 0) atomicAdd(&g_level_tasks[l], (unsigned long long)k);
+#endif
 
             // ---- Process
             const bool F = process<D>(P, S, l, v, src, has, lane, wacc);
+#ifdef GM_LEVEL_STATS
+            if (lane == 0) atomicAdd(&g_level_pass[l], (unsigned long long)__popc(__ballot_sync(FULL, F)));
+            else __ballot_sync(FULL, F);
+#endif
             my_words += wacc + (has ? 1u : 0u);
             wacc = 0;
+            if (!ENUM && P.bulk_two && l == last - 2) {
+                // pair counting: both remaining levels of every partial match at once
+                my_count += count_two<D>(P, S, l, v, src, F, lane, wacc);
+                __syncwarp();
+                continue;
+            }
             if (l == last) {
                 if (ENUM) {
                     const uint32_t fm = __ballot_sync(FULL, F);
@@ -1098,6 +1228,11 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         done = true;
     }
 
+    // a query vertex without candidates (e.g. a label absent from G): no embeddings, and the
+    // search kernels never see a label outside [0, S)
+    for (uint32_t u = 0; u < p->nq && !done; ++u)
+        if (p->cand_count[u] == 0) { total = 0; done = true; }
+
     // ---- initialization phase: BFS to tau partial matches (§4.3)
     while (!done) {
         if (P_n == 0) { total = 0; done = true; break; }
@@ -1195,6 +1330,30 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 P.last_ka = P.last_sb ? (uint32_t)__builtin_popcount(P.last_same & P.last_adj & below) : 0u;
             }
         }
+        {   // pair counting: phi[last-1], phi[last] each with one backward neighbour, not adjacent,
+            // no symmetry-breaking bounds and no filter test on either (both are implied)
+            const uint32_t last = p->nq - 1;
+            if (P.bulk_last && last >= 2 && !(o.flags & GM_FLAG_NO_PAIR_COUNT) &&
+                __builtin_popcount(p->bw[last - 1]) == 1 && !((p->bw[last] >> (last - 1)) & 1u) &&
+                !(P.sb_gt[last] | P.sb_lt[last] | P.sb_gt[last - 1] | P.sb_lt[last - 1]) &&
+                !((P.cand_needed >> (last - 1)) & 3u)) {
+                const uint32_t b6 = (uint32_t)__builtin_ctz(p->bw[last - 1]), b7 = P.last_b;
+                const uint32_t l = last - 2;
+                P.bulk_two = 1;
+                P.two_b6 = b6;
+                P.two_b7 = b7;
+                for (uint32_t i = 0; i <= l; ++i) {
+                    const uint32_t ui = p->order[i];
+                    if (i != b6 && p->qlab[ui] == p->qlab[p->order[last - 1]]) P.two_same6 |= 1u << i;
+                    if (i != b7 && p->qlab[ui] == p->qlab[p->order[last]]) P.two_same7 |= 1u << i;
+                    if ((p->qadj[p->order[b6]] >> ui) & 1u) P.two_adj6 |= 1u << i;
+                    if ((p->qadj[p->order[b7]] >> ui) & 1u) P.two_adj7 |= 1u << i;
+                }
+                const uint32_t need = (b6 < l ? 1u << b6 : 0u) | (b7 < l ? 1u << b7 : 0u) |
+                                      ((P.two_same6 | P.two_same7) & ((1u << l) - 1));
+                P.two_low = need ? (uint32_t)__builtin_ctz(need) : l;
+            }
+        }
         GM_CK(cudaEventRecord(d0e, st));
         const uint32_t nq = p->nq;
         if (nq <= 8)
@@ -1221,6 +1380,19 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         rs.donations = h.donations;
         rs.timed_out = h.abort ? 1 : 0;
         GM_CK(cudaEventElapsedTime(&rs.dfs_ms, d0e, d1e));
+#ifdef GM_LEVEL_STATS
+        {
+            unsigned long long lt[32], lp[32];
+            GM_CK(cudaMemcpyFromSymbol(lt, g_level_tasks, sizeof(lt)));
+            GM_CK(cudaMemcpyFromSymbol(lp, g_level_pass, sizeof(lp)));
+            fprintf(stderr, "[level stats] d0=%u bulk_last=%u:", d, P.bulk_last);
+            for (uint32_t i = 0; i < p->nq; ++i) fprintf(stderr, " L%u %.3g/%.3g", i, (double)lt[i], (double)lp[i]);
+            fprintf(stderr, "\n");
+            memset(lt, 0, sizeof(lt));
+            GM_CK(cudaMemcpyToSymbol(g_level_tasks, lt, sizeof(lt)));
+            GM_CK(cudaMemcpyToSymbol(g_level_pass, lt, sizeof(lt)));
+        }
+#endif
     }
     if (use_sb && __builtin_mul_overflow(total, (unsigned long long)p->aut, &total))   // one per Aut(Q)-orbit
         overflow = true;

@@ -179,6 +179,41 @@ def test_set_count_trees_same_labels(gm, seed):
         assert gm.gm_count(p, tau=tau, set_count=False)[0] == ref
 
 
+@pytest.mark.parametrize("seed", range(24))
+def test_pair_count_two_leaves(gm, seed):
+    """Pair counting: queries whose last two order positions are leaves with one backward
+    neighbour each (same or different parents, same or different labels), on power-law graphs
+    with few labels, with the hub index forced on (intersection through bitmaps), default, and
+    off (binary search); with and without symmetry breaking; against the oracle and against
+    the one-level (set_count) and task-per-candidate paths."""
+    nl = [1, 2, 3][seed % 3]
+    n, s, d = gi.rmat_edges(8 + seed % 2, 8, seed)
+    lab = gi.uniform_labels(n, nl, seed)
+    rs = np.random.default_rng(seed + 7)
+    k = 4 + seed % 3
+    core = [(int(rs.integers(0, v)), v) for v in range(1, k - 2)]          # a tree on 0..k-3
+    extra = [(a, b) for a in range(k - 2) for b in range(a + 1, k - 2) if rs.random() < 0.3]
+    p6 = int(rs.integers(0, k - 2))
+    p7 = p6 if seed % 4 == 0 else int(rs.integers(0, k - 2))
+    edges = sorted(set(core + extra + [(p6, k - 2), (p7, k - 1)]))
+    labels = rs.integers(0, nl, k).tolist()
+    if seed % 2:
+        labels[k - 1] = labels[k - 2]              # same-label leaves: the intersection term
+    q = gi.Query(k, edges, labels)
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    ref = og.count(q)
+    order = list(range(k))                         # the two leaves last
+    for budget, mindeg in ((64 << 20, 2), (64 << 20, 64), (0, 64)):
+        g.build_hubs(budget, mindeg)
+        p = gm.gm_plan_query(g, q, order=order)
+        for tau in (1, 10 ** 6):
+            assert gm.gm_count(p, tau=tau)[0] == ref
+            assert gm.gm_count(p, tau=tau, symmetry=False)[0] == ref
+        assert gm.gm_count(p, pair_count=False, symmetry=False)[0] == ref
+        assert gm.gm_count(p, set_count=False, symmetry=False)[0] == ref
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_enumerate_random_small(gm, seed):
     nl = [1, 2, 3][seed % 3]
