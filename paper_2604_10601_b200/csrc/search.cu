@@ -257,7 +257,7 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 // that leave most of the warp idle; ncu measured 12 active lanes/warp before).
 template <int D>
 __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
-                                        bool has, uint32_t lane, uint32_t &words) {
+                                        bool has, uint32_t lane, bool par, uint32_t &words) {
     // The candidate-bitmap word is loaded first and tested after the chain walk, so its L2
     // round trip overlaps the walk; it still gates the (costlier) adjacency probes.
     uint32_t cword = 0xffffffffu;
@@ -274,17 +274,27 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     // deepest such level, uniformly across lanes (P.walk_low[l]).
     const uint32_t eq = P.same_lab[l], gt = P.sb_gt[l], lt = P.sb_lt[l];
     const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
-    uint32_t p = src;
-    int k = 0;
-    // (ordering hub checks first measured 1-7 % slower on rmat18 dense queries: pairs of
-    // mixed hub/search probes overlap better)
-    for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
-        const uint32_t w = S.v[i][p];
-        if ((eq >> i) & 1u) ok = ok && (w != v);
-        if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
-        if ((lt >> i) & 1u) ok = ok && (v < w);
-        if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
-        p = S.pid[i][p];
+    // par: the set-counting level, whose checks prep_last stored per parent lane (S.chk[.][src]).
+    // There, injectivity only needs the same-label images that are not backward neighbours
+    // (v in N(w) implies v != w), and the symmetry-breaking bounds were applied to the slice
+    // by generate().  Elsewhere one walk up the pid chain collects the checks per task.
+    const uint32_t ccol = par ? src : lane;
+    if (par) {
+        const int neq = __popc(eq & ~P.bw[l]);
+        for (int e = 0; e < neq; ++e) ok = ok && (S.chk[nchk + e][src] != v);
+    } else {
+        uint32_t p = src;
+        int k = 0;
+        // (ordering hub checks first measured 1-7 % slower on rmat18 dense queries: pairs of
+        // mixed hub/search probes overlap better)
+        for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
+            const uint32_t w = S.v[i][p];
+            if ((eq >> i) & 1u) ok = ok && (w != v);
+            if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
+            if ((lt >> i) & 1u) ok = ok && (v < w);
+            if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
+            p = S.pid[i][p];
+        }
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
     // Two checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
@@ -293,8 +303,8 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     for (int c = 0; c < nchk; c += 2) {
         if (!__any_sync(FULL, ok)) break;
         const bool two = c + 1 < nchk;
-        const uint32_t w0 = S.chk[c][lane];
-        const uint32_t w1 = two ? S.chk[c + 1][lane] : 0u;
+        const uint32_t w0 = S.chk[c][ccol];
+        const uint32_t w1 = two ? S.chk[c + 1][ccol] : 0u;
         bool r0 = true, r1 = true, need0 = false, need1 = false;
         uint32_t b0 = 0, n0 = 0, b1 = 0, n1 = 0;
         if (ok) {
@@ -366,9 +376,17 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     const uint32_t gt = P.sb_gt[l + 1], lt = P.sb_lt[l + 1];
     uint32_t mb = 0, lb = 0, ub = 0xffffffffu;
     int k = 0, ka = 0;
+    // the checks of this level's tasks, per parent (process() reads them by src instead of
+    // walking the chain per task): backward images other than the slice's source, then the
+    // same-label images that are not backward neighbours (injectivity)
+    const uint32_t chkm = P.bw[l] & ~(1u << S.cs[l][lane]), eqm = P.same_lab[l] & ~P.bw[l];
+    const int nchk = __popc(P.bw[l]) - 1;
+    int kc = 0, ke = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.last_low; --i) {
         const uint32_t w = S.v[i][p];
+        if ((chkm >> i) & 1u) { S.chk[kc][lane] = w; ++kc; }
+        if ((eqm >> i) & 1u) { S.chk[nchk + ke][lane] = w; ++ke; }
         if (i == b) mb = w;
         if ((test >> i) & 1u) { S.lastw[k][lane] = w; ++k; }
         if ((known >> i) & 1u) { S.lastw[P.last_k + ka][lane] = w; ++ka; }
@@ -764,7 +782,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
 #endif
 
             // ---- Process
-            const bool F = process<D>(P, S, l, v, src, has, lane, wacc);
+            const bool F = process<D>(P, S, l, v, src, has, lane, !ENUM && P.bulk_last && l == last - 1, wacc);
 #ifdef GM_LEVEL_STATS
             if (lane == 0) atomicAdd(&g_level_pass[l], (unsigned long long)__popc(__ballot_sync(FULL, F)));
             else __ballot_sync(FULL, F);
@@ -1325,6 +1343,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 P.last_sb = (P.sb_gt[last] | P.sb_lt[last]) ? 1u : 0u;
                 uint32_t need = (b < l ? 1u << b : 0u) | (P.last_same & ~P.last_adj & below);
                 if (P.last_sb) need |= (P.last_same & P.last_adj & below) | ((P.sb_gt[last] | P.sb_lt[last]) & below);
+                need |= (p->bw[l] | P.same_lab[l]) & below;   // prep_last's per-parent check lists
                 P.last_low = need ? (uint32_t)__builtin_ctz(need) : l;
                 P.last_k = (uint32_t)__builtin_popcount(P.last_same & ~P.last_adj & below);
                 P.last_ka = P.last_sb ? (uint32_t)__builtin_popcount(P.last_same & P.last_adj & below) : 0u;
