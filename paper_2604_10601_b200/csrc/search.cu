@@ -368,7 +368,8 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 // level l = last-1 is entered (prep_last), not once per task: M[b] when b < l, and the
 // same-label images not adjacent to phi[b] in Q (those need an adjacency test).
 template <int D>
-__device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane) {
+__device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane,
+                                          uint32_t &words) {
     if (!valid) return;
     const int b = (int)P.last_b;
     const uint32_t test = P.last_same & ~P.last_adj;
@@ -397,6 +398,18 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     S.lastmb[lane] = mb;
     S.lastlb[lane] = lb;
     S.lastub[lane] = ub;
+    if (b < l && !P.last_sb) {
+        // M[b] is fixed for this parent: the count of every task is this constant minus (at
+        // most) the task's own vertex; keep it in lastlb (bounds are unused without SB)
+        const uint32_t lab = P.lab[l + 1];
+        const uint32_t row = mb * P.S + lab;
+        uint32_t cnt = ld_nc(P.offs + row + 1) - ld_nc(P.offs + row) -
+                       (uint32_t)__popc(P.last_same & P.last_adj & ((2u << l) - 1));
+        words += 2;
+        for (int c = 0; c < k; ++c)
+            if (has_edge(P, mb, P.lab[b], S.lastw[c][lane], lab, words)) --cnt;
+        S.lastlb[lane] = cnt;
+    }
 }
 
 template <int D>
@@ -406,6 +419,11 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
     const uint32_t mb = (int)P.last_b == l ? v : S.lastmb[src];   // M[b]
     const uint32_t lb_lab = P.lab[P.last_b];                       // L(M[b])
+    if (!P.last_sb && (int)P.last_b < l) {   // parent-constant part precomputed by prep_last
+        uint32_t cnt = S.lastlb[src];
+        if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lb_lab, v, lab, words)) --cnt;
+        return cnt;
+    }
     const uint32_t row = mb * P.S + lab;
     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
     words += 2;
@@ -626,7 +644,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
-                if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, d0, valid, lane);
+                if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, d0, valid, lane, wacc);
                 base = d0; l = d0;
                 got = true;
                 break;
@@ -645,7 +663,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
                     __threadfence();
                     ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                 }
-                if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, depth, lane == 0, lane);
+                if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, depth, lane == 0, lane, wacc);
                 base = (int)depth; l = (int)depth;
                 got = true;
                 break;
@@ -831,7 +849,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
             if (!fm) continue;
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
             generate<D>(P, S, l + 1, F, lane, wacc);
-            if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, l + 1, F, lane);
+            if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, l + 1, F, lane, wacc);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
             __syncwarp();
             ++l;
