@@ -115,6 +115,8 @@ struct SearchParams {
     uint32_t two_same6, two_same7;  // positions i <= last-2 (i != b) labelled like phi[last-1] / phi[last]
     uint32_t two_adj6, two_adj7;    // ... whose query vertex is adjacent to phi[b6] / phi[b7]
     uint32_t two_low;           // deepest level count_two's walk visits
+    uint32_t par_level;         // level whose checks are kept per parent (prep_checks), or ~0u
+    uint32_t par_low;           // deepest level prep_checks visits
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
@@ -355,6 +357,27 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     return ok;
 }
 
+// The checks of the tasks at level l = P.par_level (the level holding almost all tasks: the
+// set-counting level, else the last), recorded once per parent lane when the level is
+// entered, so that process() reads them by src instead of walking the pid chain per task:
+// the backward images other than the slice's source, then the same-label images that are
+// not backward neighbours (the only ones injectivity must compare: v in N(w) implies v != w).
+template <int D>
+__device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> &S, int l, bool valid,
+                                            uint32_t lane) {
+    if (!valid) return;
+    const uint32_t chkm = P.bw[l] & ~(1u << S.cs[l][lane]), eqm = P.same_lab[l] & ~P.bw[l];
+    const int nchk = __popc(P.bw[l]) - 1;
+    int kc = 0, ke = 0;
+    uint32_t p = lane;
+    for (int i = l - 1; i >= (int)P.par_low; --i) {
+        const uint32_t w = S.v[i][p];
+        if ((chkm >> i) & 1u) { S.chk[kc][lane] = w; ++kc; }
+        if ((eqm >> i) & 1u) { S.chk[nchk + ke][lane] = w; ++ke; }
+        p = S.pid[i][p];
+    }
+}
+
 // Last-level set counting (count mode): when phi[last] has ONE
 // backward neighbour phi[b], the valid extensions of a partial match M of depth last are
 // exactly the vertices of N_{L(phi[last])}(M[b]) not already in M (adjacency is the only
@@ -377,17 +400,9 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     const uint32_t gt = P.sb_gt[l + 1], lt = P.sb_lt[l + 1];
     uint32_t mb = 0, lb = 0, ub = 0xffffffffu;
     int k = 0, ka = 0;
-    // the checks of this level's tasks, per parent (process() reads them by src instead of
-    // walking the chain per task): backward images other than the slice's source, then the
-    // same-label images that are not backward neighbours (injectivity)
-    const uint32_t chkm = P.bw[l] & ~(1u << S.cs[l][lane]), eqm = P.same_lab[l] & ~P.bw[l];
-    const int nchk = __popc(P.bw[l]) - 1;
-    int kc = 0, ke = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.last_low; --i) {
         const uint32_t w = S.v[i][p];
-        if ((chkm >> i) & 1u) { S.chk[kc][lane] = w; ++kc; }
-        if ((eqm >> i) & 1u) { S.chk[nchk + ke][lane] = w; ++ke; }
         if (i == b) mb = w;
         if ((test >> i) & 1u) { S.lastw[k][lane] = w; ++k; }
         if ((known >> i) & 1u) { S.lastw[P.last_k + ka][lane] = w; ++ka; }
@@ -644,6 +659,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
+                if (d0 == (int)P.par_level) prep_checks<D>(P, S, d0, valid, lane);
                 if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, d0, valid, lane, wacc);
                 base = d0; l = d0;
                 got = true;
@@ -663,6 +679,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
                     __threadfence();
                     ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                 }
+                if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, depth, lane == 0, lane);
                 if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, depth, lane == 0, lane, wacc);
                 base = (int)depth; l = (int)depth;
                 got = true;
@@ -800,7 +817,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
 #endif
 
             // ---- Process
-            const bool F = process<D>(P, S, l, v, src, has, lane, !ENUM && P.bulk_last && l == last - 1, wacc);
+            const bool F = process<D>(P, S, l, v, src, has, lane, l == (int)P.par_level, wacc);
 #ifdef GM_LEVEL_STATS
             if (lane == 0) atomicAdd(&g_level_pass[l], (unsigned long long)__popc(__ballot_sync(FULL, F)));
             else __ballot_sync(FULL, F);
@@ -849,6 +866,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
             if (!fm) continue;
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
             generate<D>(P, S, l + 1, F, lane, wacc);
+            if (l + 1 == (int)P.par_level) prep_checks<D>(P, S, l + 1, F, lane);
             if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, l + 1, F, lane, wacc);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
             __syncwarp();
@@ -1361,7 +1379,6 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 P.last_sb = (P.sb_gt[last] | P.sb_lt[last]) ? 1u : 0u;
                 uint32_t need = (b < l ? 1u << b : 0u) | (P.last_same & ~P.last_adj & below);
                 if (P.last_sb) need |= (P.last_same & P.last_adj & below) | ((P.sb_gt[last] | P.sb_lt[last]) & below);
-                need |= (p->bw[l] | P.same_lab[l]) & below;   // prep_last's per-parent check lists
                 P.last_low = need ? (uint32_t)__builtin_ctz(need) : l;
                 P.last_k = (uint32_t)__builtin_popcount(P.last_same & ~P.last_adj & below);
                 P.last_ka = P.last_sb ? (uint32_t)__builtin_popcount(P.last_same & P.last_adj & below) : 0u;
@@ -1389,6 +1406,16 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 const uint32_t need = (b6 < l ? 1u << b6 : 0u) | (b7 < l ? 1u << b7 : 0u) |
                                       ((P.two_same6 | P.two_same7) & ((1u << l) - 1));
                 P.two_low = need ? (uint32_t)__builtin_ctz(need) : l;
+            }
+        }
+        {   // per-parent check lists at the level holding almost all tasks (prep_checks); none
+            // with pair counting (its levels have no checks)
+            const uint32_t last = p->nq - 1;
+            P.par_level = P.bulk_two ? ~0u : (P.bulk_last ? last - 1 : last);
+            if (P.par_level != ~0u) {
+                const uint32_t l = P.par_level;
+                const uint32_t need = (p->bw[l] | P.same_lab[l]) & ((1u << l) - 1);
+                P.par_low = need ? (uint32_t)__builtin_ctz(need) : l;
             }
         }
         GM_CK(cudaEventRecord(d0e, st));
