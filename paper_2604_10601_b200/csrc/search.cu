@@ -535,6 +535,27 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
             __syncwarp();
             uint32_t ci = 0, cj = 0;
             while (true) {
+                // fast path: the cursor's list alone fills the round (long lists against a hub)
+                const uint32_t sl_ci = __shfl_sync(FULL, sl, ci & 31);
+                if (ci < 32 && sl_ci - cj >= 32) {
+                    const uint32_t f_sb = __shfl_sync(FULL, sb, ci), f_gb = __shfl_sync(FULL, gb, ci);
+                    const uint32_t f_ge = __shfl_sync(FULL, ge, ci), f_gown = __shfl_sync(FULL, gown, ci);
+                    const uint32_t x = ld_nc(P.nbr + f_sb + cj + lane);
+                    ++words;
+                    bool hit;
+                    if (f_gown < P.nhubs) {
+                        ++words;
+                        hit = (ld_nc(P.hub_bits + (unsigned long long)f_gown * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+                    } else {
+                        hit = contains(P.nbr, f_gb, f_ge, x, words);
+                    }
+                    const uint32_t h = __popc(__ballot_sync(FULL, hit));
+                    if (lane == 0) S.tacc[ci] += h;
+                    __syncwarp();
+                    cj += 32;
+                    if (cj == sl_ci) { ++ci; cj = 0; }
+                    continue;
+                }
                 uint32_t rem = lane >= ci ? sl - (lane == ci ? cj : 0u) : 0u;
                 const uint32_t r32 = min(rem, 32u);
                 uint32_t incl = r32;
