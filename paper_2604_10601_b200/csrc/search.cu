@@ -540,19 +540,27 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                 if (ci < 32 && sl_ci - cj >= 32) {
                     const uint32_t f_sb = __shfl_sync(FULL, sb, ci), f_gb = __shfl_sync(FULL, gb, ci);
                     const uint32_t f_ge = __shfl_sync(FULL, ge, ci), f_gown = __shfl_sync(FULL, gown, ci);
+                    // two elements per lane when 64 remain: two independent probes in flight
+                    const uint32_t step = sl_ci - cj >= 64 ? 64u : 32u;
                     const uint32_t x = ld_nc(P.nbr + f_sb + cj + lane);
-                    ++words;
-                    bool hit;
+                    const uint32_t x2 = step == 64 ? ld_nc(P.nbr + f_sb + cj + 32 + lane) : 0u;
+                    words += step >> 5;
+                    bool hit, hit2 = false;
                     if (f_gown < P.nhubs) {
-                        ++words;
-                        hit = (ld_nc(P.hub_bits + (unsigned long long)f_gown * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+                        words += step >> 5;
+                        const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
+                        const uint32_t w1 = ld_nc(row + (x >> 5));
+                        const uint32_t w2 = step == 64 ? ld_nc(row + (x2 >> 5)) : 0u;
+                        hit = (w1 >> (x & 31)) & 1u;
+                        hit2 = step == 64 && ((w2 >> (x2 & 31)) & 1u);
                     } else {
                         hit = contains(P.nbr, f_gb, f_ge, x, words);
+                        if (step == 64) hit2 = contains(P.nbr, f_gb, f_ge, x2, words);
                     }
-                    const uint32_t h = __popc(__ballot_sync(FULL, hit));
+                    const uint32_t h = __popc(__ballot_sync(FULL, hit)) + __popc(__ballot_sync(FULL, hit2));
                     if (lane == 0) S.tacc[ci] += h;
                     __syncwarp();
-                    cj += 32;
+                    cj += step;
                     if (cj == sl_ci) { ++ci; cj = 0; }
                     continue;
                 }
