@@ -1411,6 +1411,11 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 P.last_low = need ? (uint32_t)__builtin_ctz(need) : l;
                 P.last_k = (uint32_t)__builtin_popcount(P.last_same & ~P.last_adj & below);
                 P.last_ka = P.last_sb ? (uint32_t)__builtin_popcount(P.last_same & P.last_adj & below) : 0u;
+                // The candidate-filter test of phi[last-1] is subsumed by the set count: its only
+                // possible forward neighbour is phi[last], so a candidate the (sound) filter
+                // rejects has no valid extension and count_last returns exactly 0 for it.
+                // Skipping the test takes a dependent bitmap load off every task of the level.
+                P.cand_needed &= ~(1u << l);
             }
         }
         {   // pair counting: phi[last-1], phi[last] each with one backward neighbour, not adjacent,
