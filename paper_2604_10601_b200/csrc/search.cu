@@ -115,6 +115,7 @@ struct SearchParams {
     uint32_t two_same6, two_same7;  // positions i <= last-2 (i != b) labelled like phi[last-1] / phi[last]
     uint32_t two_adj6, two_adj7;    // ... whose query vertex is adjacent to phi[b6] / phi[b7]
     uint32_t two_low;           // deepest level count_two's walk visits
+    uint32_t two_walk;          // 1: a per-task row (b6 or b7 == last-2) has same-label images below
     uint32_t par_level;         // level whose checks are kept per parent (prep_checks), or ~0u
     uint32_t par_low;           // deepest level prep_checks visits
     uint32_t *out;              // enumerate rows (nq words each)
@@ -474,6 +475,53 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     return cnt;
 }
 
+// Per-parent part of pair counting, run when level l = last-2 is entered: M[b6], M[b7] and
+// the bounds of A = N(M[b6]) and R = N(M[b7]) when those are parent images (b < l), and the
+// mapped same-label images (levels < l) inside A, inside R and inside both.  The images'
+// membership is only summed here when no per-task row needs them (!P.two_walk).
+template <int D>
+__device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane,
+                                         uint32_t &words) {
+    if (!valid) return;
+    const uint32_t lab6 = P.lab[l + 1], lab7 = P.lab[l + 2];
+    const int b6 = (int)P.two_b6, b7 = (int)P.two_b7;
+    uint32_t m6 = 0, m7 = 0;
+    uint32_t p = lane;
+    for (int i = l - 1; i >= (int)P.two_low; --i) {
+        const uint32_t w = S.v[i][p];
+        if (i == b6) m6 = w;
+        if (i == b7) m7 = w;
+        p = S.pid[i][p];
+    }
+    S.lastw[0][lane] = m6;
+    S.lastw[1][lane] = m7;
+    if (b6 < l) {
+        const uint32_t ra = m6 * P.S + lab6;
+        S.lastw[2][lane] = ld_nc(P.offs + ra); S.lastw[3][lane] = ld_nc(P.offs + ra + 1);
+        words += 2;
+    }
+    if (b7 < l) {
+        const uint32_t rr = m7 * P.S + lab7;
+        S.lastw[4][lane] = ld_nc(P.offs + rr); S.lastw[5][lane] = ld_nc(P.offs + rr + 1);
+        words += 2;
+    }
+    uint32_t inA = 0, inR = 0, inAR = 0;
+    if (!P.two_walk) {
+        p = lane;
+        for (int i = l - 1; i >= (int)P.two_low; --i) {
+            const uint32_t w = S.v[i][p];
+            bool a = false, r = false;
+            if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge(P, m6, P.lab[b6], w, lab6, words);
+            if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge(P, m7, P.lab[b7], w, lab7, words);
+            inA += a; inR += r; inAR += a && r;
+            p = S.pid[i][p];
+        }
+    }
+    S.lastmb[lane] = inA;
+    S.lastlb[lane] = inR;
+    S.lastub[lane] = inAR;
+}
+
 // Pair counting (count mode): when phi[last-1] and phi[last] each
 // have ONE backward neighbour, b6 and b7, and are not adjacent to each other, the embeddings
 // extending a partial match M of depth last-1 (levels 0..l, l = last-2) are the pairs
@@ -495,27 +543,32 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
     const int b6 = (int)P.two_b6, b7 = (int)P.two_b7;
     uint32_t m6 = v, m7 = v, a0 = 0, a1 = 0, r0 = 0, r1 = 0, inA = 0, inR = 0, inAR = 0;
     if (F) {
-        uint32_t p = src;
-        for (int i = l - 1; i >= (int)P.two_low; --i) {   // M[b6], M[b7]
-            const uint32_t w = S.v[i][p];
-            if (i == b6) m6 = w;
-            if (i == b7) m7 = w;
-            p = S.pid[i][p];
-        }
-        const uint32_t ra = m6 * P.S + lab6, rr = m7 * P.S + lab7;
-        a0 = ld_nc(P.offs + ra); a1 = ld_nc(P.offs + ra + 1);
-        r0 = ld_nc(P.offs + rr); r1 = ld_nc(P.offs + rr + 1);
-        words += 4;
+        // parent-constant parts from prep_two (lastw rows 0-5, lastmb/lb/ub); the row of a
+        // backward neighbour mapped at this level (b == l, i.e. v) is read per task
+        if (b6 < l) { m6 = S.lastw[0][src]; a0 = S.lastw[2][src]; a1 = S.lastw[3][src]; }
+        else { const uint32_t ra = v * P.S + lab6; a0 = ld_nc(P.offs + ra); a1 = ld_nc(P.offs + ra + 1); words += 2; }
+        if (b7 < l) { m7 = S.lastw[1][src]; r0 = S.lastw[4][src]; r1 = S.lastw[5][src]; }
+        else { const uint32_t rr = v * P.S + lab7; r0 = ld_nc(P.offs + rr); r1 = ld_nc(P.offs + rr + 1); words += 2; }
         // mapped vertices inside A and R: only same-label ones can be; surely if their query
         // vertex is adjacent to phi[b] in Q, else one edge test
-        p = src;
-        for (int i = l; i >= (int)P.two_low; --i) {
-            const uint32_t w = i == l ? v : S.v[i][p];
+        if (P.two_walk) {       // a per-task row with same-label images below l: test them all here
+            uint32_t p = src;
+            for (int i = l - 1; i >= (int)P.two_low; --i) {
+                const uint32_t w = S.v[i][p];
+                bool a = false, r = false;
+                if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge(P, m6, P.lab[b6], w, lab6, words);
+                if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge(P, m7, P.lab[b7], w, lab7, words);
+                inA += a; inR += r; inAR += a && r;
+                p = S.pid[i][p];
+            }
+        } else {                // every image below l was tested once per parent
+            inA = S.lastmb[src]; inR = S.lastlb[src]; inAR = S.lastub[src];
+        }
+        {   // the task's own vertex (never in a row it owns: same6/same7 exclude b6/b7)
             bool a = false, r = false;
-            if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge(P, m6, P.lab[b6], w, lab6, words);
-            if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge(P, m7, P.lab[b7], w, lab7, words);
+            if ((P.two_same6 >> l) & 1u) a = ((P.two_adj6 >> l) & 1u) || has_edge(P, m6, P.lab[b6], v, lab6, words);
+            if ((P.two_same7 >> l) & 1u) r = ((P.two_adj7 >> l) & 1u) || has_edge(P, m7, P.lab[b7], v, lab7, words);
             inA += a; inR += r; inAR += a && r;
-            if (i < l) p = S.pid[i][p];
         }
     }
     const unsigned long long nV = (unsigned long long)(a1 - a0 - inA), nB = (unsigned long long)(r1 - r0 - inR);
@@ -689,6 +742,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
                 if (d0 == (int)P.par_level) prep_checks<D>(P, S, d0, valid, lane);
+                if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, d0, valid, lane, wacc);
                 if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, d0, valid, lane, wacc);
                 base = d0; l = d0;
                 got = true;
@@ -709,6 +763,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
                     ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                 }
                 if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, depth, lane == 0, lane);
+                if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, depth, lane == 0, lane, wacc);
                 if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, depth, lane == 0, lane, wacc);
                 base = (int)depth; l = (int)depth;
                 got = true;
@@ -896,6 +951,7 @@ __global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) 
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
             generate<D>(P, S, l + 1, F, lane, wacc);
             if (l + 1 == (int)P.par_level) prep_checks<D>(P, S, l + 1, F, lane);
+            if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, l + 1, F, lane, wacc);
             if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, l + 1, F, lane, wacc);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
             __syncwarp();
@@ -1437,15 +1493,17 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                     if ((p->qadj[p->order[b6]] >> ui) & 1u) P.two_adj6 |= 1u << i;
                     if ((p->qadj[p->order[b7]] >> ui) & 1u) P.two_adj7 |= 1u << i;
                 }
+                const uint32_t below = (1u << l) - 1;
                 const uint32_t need = (b6 < l ? 1u << b6 : 0u) | (b7 < l ? 1u << b7 : 0u) |
-                                      ((P.two_same6 | P.two_same7) & ((1u << l) - 1));
+                                      ((P.two_same6 | P.two_same7) & below);
                 P.two_low = need ? (uint32_t)__builtin_ctz(need) : l;
+                P.two_walk = ((b6 == l && (P.two_same6 & below)) || (b7 == l && (P.two_same7 & below))) ? 1u : 0u;
             }
         }
         {   // per-parent check lists at the level holding almost all tasks (prep_checks); none
             // with pair counting (its levels have no checks)
             const uint32_t last = p->nq - 1;
-            P.par_level = P.bulk_two ? ~0u : (P.bulk_last ? last - 1 : last);
+            P.par_level = P.bulk_two ? last - 2 : (P.bulk_last ? last - 1 : last);
             if (P.par_level != ~0u) {
                 const uint32_t l = P.par_level;
                 const uint32_t need = (p->bw[l] | P.same_lab[l]) & ((1u << l) - 1);
