@@ -1154,7 +1154,7 @@ template <int D>
 static size_t stack_bytes() { return sizeof(WarpStack<D>); }
 
 template <int D, bool ENUM>
-static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, cudaStream_t st,
+static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
     const size_t smem = stack_bytes<D>() * wpb;
     auto kern = k_dfs<D, ENUM>;
@@ -1167,7 +1167,8 @@ static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, cudaS
     // pool items per fetch: 32 (a full warp of parent lanes) when the pool is large; fewer
     // when it is small, so that every warp gets some initial work (§4.3).
     const unsigned long long nwarps = (unsigned long long)grid * wpb;
-    const unsigned long long per_warp = P.pool_size / (4 * nwarps);
+    // with a pool counter shared by `sharers` ranks, all of their warps draw from this pool
+    const unsigned long long per_warp = P.pool_size / (4 * nwarps * std::max<uint32_t>(1, sharers));
     P.batch = (uint32_t)std::max<unsigned long long>(1, std::min<unsigned long long>(32, per_warp));
     kern<<<grid, wpb * 32, smem, st>>>(P);
     GM_CK(cudaGetLastError());
@@ -1513,14 +1514,14 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         GM_CK(cudaEventRecord(d0e, st));
         const uint32_t nq = p->nq;
         if (nq <= 8)
-            rc = enumerate ? launch_dfs<8, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block)
-                           : launch_dfs<8, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block);
+            rc = enumerate ? launch_dfs<8, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block)
+                           : launch_dfs<8, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block);
         else if (nq <= 16)
-            rc = enumerate ? launch_dfs<16, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block)
-                           : launch_dfs<16, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block);
+            rc = enumerate ? launch_dfs<16, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block)
+                           : launch_dfs<16, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block);
         else
-            rc = enumerate ? launch_dfs<32, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block)
-                           : launch_dfs<32, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, st, &rs.grid, &rs.block);
+            rc = enumerate ? launch_dfs<32, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block)
+                           : launch_dfs<32, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block);
         if (rc) return rc;
         ++launches;
         rs.dfs_launches = 1;
