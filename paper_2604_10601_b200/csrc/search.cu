@@ -42,6 +42,9 @@
 namespace gm {
 
 constexpr uint32_t FULL = 0xffffffffu;
+#ifndef GM_CHK_ORDER
+#define GM_CHK_ORDER 1
+#endif
 #ifndef GM_VHUB
 #define GM_VHUB 1
 #endif
@@ -377,6 +380,16 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
         if ((eqm >> i) & 1u) { S.chk[nchk + ke][lane] = w; ++ke; }
         p = S.pid[i][p];
     }
+#if GM_CHK_ORDER
+    // most selective check first: larger device id = lower degree = fewer neighbours, so more
+    // tasks fail early and whole warps leave the probe loop sooner
+    for (int a = 1; a < nchk; ++a) {
+        const uint32_t x = S.chk[a][lane];
+        int b = a - 1;
+        while (b >= 0 && S.chk[b][lane] < x) { S.chk[b + 1][lane] = S.chk[b][lane]; --b; }
+        S.chk[b + 1][lane] = x;
+    }
+#endif
 }
 
 // Last-level set counting (count mode): when phi[last] has ONE
