@@ -624,3 +624,32 @@ def test_config5_local_parity(gm):
                 i = np.searchsorted(nb, r[b])
                 assert i < len(nb) and nb[i] == r[b]
     assert checked >= 12 and nonzero >= 3
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_pool_depth_sweep_counting_paths(gm, seed):
+    """tau sweeps the depth of the initial pool (Alg. 2 line 1, §4.3) across every level, so the
+    DFS starts at, below and above the pair-counting (last-2) and set-counting (last-1)
+    levels, with and without stealing; every count equals the oracle's."""
+    nl = 2
+    n, s, d = gi.rmat_edges(9, 8, 40 + seed)
+    lab = gi.uniform_labels(n, nl, 40 + seed)
+    rs = np.random.default_rng(60 + seed)
+    k = 5 + seed % 2
+    # a tree on 0..k-3 plus two non-adjacent leaves last (pair counting applies in the given order)
+    edges = [(int(rs.integers(0, v)), v) for v in range(1, k - 2)]
+    edges += [(int(rs.integers(0, k - 2)), k - 2), (int(rs.integers(0, k - 2)), k - 1)]
+    q = gi.Query(k, sorted(set(edges)), rs.integers(0, nl, k).tolist())
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    ref = og.count(q)
+    p = gm.gm_plan_query(g, q, order=list(range(k)))
+    depths = set()
+    for tau in (1, 4, 16, 64, 256, 1024, 4096, 16384, 65536, 10 ** 6):
+        for steal in (True, False):
+            c, st = gm.gm_count(p, tau=tau, steal=steal, symmetry=False)
+            assert c == ref, (tau, steal, st["pool_depth"])
+            depths.add(st["pool_depth"] if st["dfs_launches"] else k)
+        assert gm.gm_count(p, tau=tau)[0] == ref
+    # the DFS started below the pair-counting level and at the set-counting level (depth k-2)
+    assert min(depths) <= k - 3 and (k - 2) in depths, depths
