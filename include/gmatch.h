@@ -178,7 +178,7 @@ typedef struct {
     uint32_t root_chunk;     /* 0 = 64 */
     uint32_t steal;          /* 1 = idle-warp work stealing on (gm_default_opts), 0 = off */
     uint32_t blocks_per_sm;  /* 0 = as many as fit */
-    uint32_t warps_per_block;/* 0 = 4 */
+    uint32_t warps_per_block;/* DFS warps per block, 1..4 (0 = 4); larger: GM_ERR_ARG */
     double   time_limit_ms;  /* 0 = none; on expiry the call returns GM_TIMEOUT */
     const uint32_t *roots;   /* optional host list of DISTINCT vertices restricting phi[0]'s
                                 images to them (still filtered and rank-partitioned);

@@ -51,6 +51,7 @@ constexpr uint32_t FULL = 0xffffffffu;
 #ifndef GM_DFS_MINB
 #define GM_DFS_MINB 9
 #endif
+constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
 constexpr uint32_t kItemWords = 4 + kMaxQ;     // [depth, cb, cl, cs, prefix[kMaxQ]]
 
 // Global control block.  Every field that many warps poll or update lives on its own
@@ -689,7 +690,7 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // ------------------------------------------------------------------ DFS kernel
 
 template <int D, bool ENUM>
-__global__ void __launch_bounds__(128, GM_DFS_MINB) k_dfs(const SearchParams P) {
+__global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     WarpStack<D> &S = reinterpret_cast<WarpStack<D> *>(smem_raw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;
@@ -1255,7 +1256,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         if (!o.pool_bytes_max) o.pool_bytes_max = 1ull << 30;
     }
     GM_REQ(o.rank < o.world, GM_ERR_ARG, "rank %u >= world %u", o.rank, o.world);
-    GM_REQ(o.warps_per_block <= 32, GM_ERR_ARG, "warps_per_block > 32");
+    GM_REQ(o.warps_per_block <= kDfsMaxWarps, GM_ERR_ARG, "warps_per_block %u > %u (k_dfs launch bounds)",
+           o.warps_per_block, kDfsMaxWarps);
     GM_REQ(o.num_roots == 0 || o.roots, GM_ERR_ARG, "num_roots > 0 but roots NULL");
     const gm_graph *g = p->g;
     int dev = 0;

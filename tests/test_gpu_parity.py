@@ -653,3 +653,19 @@ def test_pool_depth_sweep_counting_paths(gm, seed):
         assert gm.gm_count(p, tau=tau)[0] == ref
     # the DFS started below the pair-counting level and at the set-counting level (depth k-2)
     assert min(depths) <= k - 3 and (k - 2) in depths, depths
+
+
+def test_launch_shape_options(gm):
+    """warps_per_block 1/2/4 and blocks_per_sm give the oracle's count; more warps per block
+    than k_dfs is compiled for is an argument error, not a failed launch."""
+    n, s, d = gi.rmat_edges(9, 8, 5)
+    lab = gi.uniform_labels(n, 2, 5)
+    q = small_random_query(5, 5, 2)
+    ref, c, st, og, g, p = run_both(gm, n, s, d, lab, 2, q)
+    assert c == ref
+    for wpb in (1, 2, 4):
+        for bps in (0, 1, 3):
+            assert gm.gm_count(p, warps_per_block=wpb, blocks_per_sm=bps, tau=16)[0] == ref
+    with pytest.raises(gm.GMError) as e:
+        gm.gm_count(p, warps_per_block=8)
+    assert "warps_per_block" in str(e.value)
