@@ -370,6 +370,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 template <int D>
 __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> &S, int l, bool valid,
                                             uint32_t lane) {
+    static_assert(GM_CHK_ROWS >= D - 2, "checks + injectivity images of a level: up to D - 2");
     if (!valid) return;
     const uint32_t chkm = P.bw[l] & ~(1u << S.cs[l][lane]), eqm = P.same_lab[l] & ~P.bw[l];
     const int nchk = __popc(P.bw[l]) - 1;
@@ -496,6 +497,7 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
 template <int D>
 __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane,
                                          uint32_t &words) {
+    static_assert(GM_LASTW_ROWS >= 6, "prep_two keeps six per-parent words in lastw");
     if (!valid) return;
     const uint32_t lab6 = P.lab[l + 1], lab7 = P.lab[l + 2];
     const int b6 = (int)P.two_b6, b7 = (int)P.two_b7;
