@@ -451,7 +451,8 @@ def main():
                    "embeddings_per_step": emb_per_step, "tau": int(args.tau), "steal": not args.no_steal,
                    "filter": "nlf", "graph": {k: ginfo[k] for k in ("n", "num_adj", "num_labels", "d_max")},
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": (f"{world} GPU(s), CSR replicated, " +
+                   "parallelism": ("1 GPU, whole pool on one device" if world == 1 else
+                                   f"{world} GPU(s), CSR replicated, " +
                                    ("pool batches claimed from one shared counter (NVLink peer atomics)"
                                     if shared_ptr is not None else "static root partition") +
                                    ", 1 all-reduce of the counts per step")},
