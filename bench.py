@@ -329,8 +329,8 @@ def main():
             e1.record(stream)
             plans.append(p)
             out.append((st, e0, e1))
-        partition.reduce_counts(counts_dev)      # the one collective of the step (N > 1)
-        return out, plans
+        halves = partition.reduce_count_halves(counts_dev)   # the one collective of the step (N > 1)
+        return out, plans, halves
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -349,13 +349,14 @@ def main():
         torch.cuda.synchronize()
         s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        res, plans = step(True)
+        res, plans, halves = step(True)
         s1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         step_ms.append(s0.elapsed_time(s1))
-        total_emb += int(counts_dev.sum().item())
+        exact = partition.count_totals(halves)       # exact uint64 sums (no int64 wrap)
+        total_emb += sum(exact)
         for i, (st, e0, e1) in enumerate(res):
             q_ms.append(e0.elapsed_time(e1))
             dfs_ms.append(st["dfs_ms"])
@@ -366,7 +367,7 @@ def main():
             timeouts += st["timed_out"]
             if k == 0:
                 per_query.append({"q": qs[i].name, "m": int(len(qs[i].edges)), "ms": round(q_ms[-1], 3),
-                                  "embeddings": int(counts_dev[i].item()), "aut": st["automorphisms"],
+                                  "embeddings": exact[i], "aut": st["automorphisms"],
                                   "dfs_ms": round(st["dfs_ms"], 3), "timed_out": st["timed_out"],
                                   "pool": st["pool_size"], "depth": st["pool_depth"],
                                   "donations": st["donations"]})
@@ -408,9 +409,8 @@ def main():
             h2d += q.edges.nbytes + q.labels.nbytes
             d2h += 8
         if world > 1:
-            t = torch.tensor(local, dtype=torch.int64, device=dev)
-            dist.all_reduce(t)
-            local = t.cpu().tolist()
+            t = torch.tensor(partition.as_int64_bits(local), dtype=torch.int64, device=dev)
+            local = partition.reduce_counts(t)
             d2h += 8 * len(qs)
         dt = time.perf_counter() - t0
         if world > 1:

@@ -38,11 +38,14 @@ def _worker(rank, world, port, out):
         for i, q in enumerate(queries):
             roots = partition.owned_roots(np.flatnonzero(lab == q.labels[0]), rank, world, chunk=16)
             counts[i] = sum(og.count(q, fixed=(0, int(v))) for v in roots)
-        partition.reduce_counts(counts)
+        exact = partition.reduce_counts(counts)
         t = partition.max_over_ranks(1.0 + rank)
+        # uint64 counts near 2^64 (stored bit for bit in int64): the exact sum exceeds int64
+        big = torch.tensor([(2**64 - 5 - (1 << 64)), 2**63 + 7 - (1 << 64), 3], dtype=torch.int64)
+        big_tot = partition.reduce_counts(big)
         if rank == 0:
             totals = [og.count(q) for q in queries]
-            out.put((counts.tolist(), totals, t))
+            out.put((counts.tolist(), totals, t, exact, big_tot))
     finally:
         dist.destroy_process_group()
 
@@ -69,6 +72,8 @@ def test_gloo_two_ranks_reduce_to_total(world):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    counts, totals, t = got
-    assert counts == totals
+    counts, totals, t, exact, big_tot = got
+    assert counts == totals and exact == totals
     assert t == float(world)      # max over ranks of 1 + rank
+    # uint64 inputs near 2^64 on every rank: exact sums, beyond the int64 range
+    assert big_tot == [world * (2**64 - 5), world * (2**63 + 7), world * 3]
