@@ -42,6 +42,10 @@
 namespace gm {
 
 constexpr uint32_t FULL = 0xffffffffu;
+// per-warp scratch rows (32 words each) after the WarpStack: rows_chk rows of check images,
+// then rows_last rows of set/pair-counting words
+#define CHK(k, x) scr[(k) * 32u + (x)]
+#define LASTW(k, x) scr[(P.rows_chk + (k)) * 32u + (x)]
 #ifndef GM_CHK_ORDER
 #define GM_CHK_ORDER 1
 #endif
@@ -120,6 +124,9 @@ struct SearchParams {
     uint32_t two_adj6, two_adj7;    // ... whose query vertex is adjacent to phi[b6] / phi[b7]
     uint32_t two_low;           // deepest level count_two's walk visits
     uint32_t two_walk;          // 1: a per-task row (b6 or b7 == last-2) has same-label images below
+    uint32_t rows_chk;          // scratch rows for check images (max checks of a task / par-level list)
+    uint32_t rows_last;         // scratch rows for set/pair-counting words
+    uint32_t warp_stride;       // bytes of shared memory per warp: WarpStack + scratch rows
     uint32_t par_level;         // level whose checks are kept per parent (prep_checks), or ~0u
     uint32_t par_low;           // deepest level prep_checks visits
     uint32_t *out;              // enumerate rows (nq words each)
@@ -197,14 +204,8 @@ struct WarpStack {
     uint32_t cl[D][32];   //                  its length
     uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
     uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
-#ifndef GM_CHK_ROWS
-#define GM_CHK_ROWS (D - 2)   // checks per task <= |bw| - 1 <= D - 2
-#endif
-#ifndef GM_LASTW_ROWS
-#define GM_LASTW_ROWS (D - 2) // set-counting images: positions < last - 1
-#endif
-    uint32_t chk[GM_CHK_ROWS][32];  // scratch: the backward-neighbour images a lane's task must be adjacent to
-    uint32_t lastw[GM_LASTW_ROWS][32];// set counting: per parent lane at level last-2, the same-label images to test
+    // (the per-warp scratch rows -- check images and set/pair-counting words -- follow the
+    // struct in shared memory, sized per query: see SearchParams.rows_chk / rows_last)
     uint32_t lastmb[32];  //               and the image of phi[last]'s backward neighbour (if < last-1)
     uint32_t lastlb[32];  //               symmetry-breaking bounds of phi[last] from levels < last-1:
     uint32_t lastub[32];  //               its image must lie in [lastlb, lastub)
@@ -263,7 +264,7 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 // searches step in lock-step until every lane is done (instead of per-lane early exits
 // that leave most of the warp idle; ncu measured 12 active lanes/warp before).
 template <int D>
-__device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
+__device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, uint32_t v, uint32_t src,
                                         bool has, uint32_t lane, bool par, uint32_t &words) {
     // The candidate-bitmap word is loaded first and tested after the chain walk, so its L2
     // round trip overlaps the walk; it still gates the (costlier) adjacency probes.
@@ -274,21 +275,21 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     }
     bool ok = has;
     const uint32_t cs = has ? S.cs[l][src] : 0u;
-    const uint32_t chk = P.bw[l] & ~(1u << cs);
+    const uint32_t chk = has ? P.bw[l] & ~(1u << cs) : 0u;   // exactly nchk images for a task
     const uint32_t lab = P.lab[l];
     // Only levels holding a backward neighbour (adjacency check) or a vertex of v's label
     // (v can only collide with a same-label image) need visiting; the walk stops at the
     // deepest such level, uniformly across lanes (P.walk_low[l]).
     const uint32_t eq = P.same_lab[l], gt = P.sb_gt[l], lt = P.sb_lt[l];
     const int nchk = __popc(P.bw[l]) - 1;           // uniform (the source level is in bw)
-    // par: the set-counting level, whose checks prep_last stored per parent lane (S.chk[.][src]).
+    // par: the set-counting level, whose checks prep_last stored per parent lane (CHK(., src)).
     // There, injectivity only needs the same-label images that are not backward neighbours
     // (v in N(w) implies v != w), and the symmetry-breaking bounds were applied to the slice
     // by generate().  Elsewhere one walk up the pid chain collects the checks per task.
     const uint32_t ccol = par ? src : lane;
     if (par) {
         const int neq = __popc(eq & ~P.bw[l]);
-        for (int e = 0; e < neq; ++e) ok = ok && (S.chk[nchk + e][src] != v);
+        for (int e = 0; e < neq; ++e) ok = ok && (CHK(nchk + e, src) != v);
     } else {
         uint32_t p = src;
         int k = 0;
@@ -299,7 +300,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
             if ((eq >> i) & 1u) ok = ok && (w != v);
             if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
             if ((lt >> i) & 1u) ok = ok && (v < w);
-            if ((chk >> i) & 1u) { S.chk[k][lane] = w; ++k; }
+            if ((chk >> i) & 1u) { CHK(k, lane) = w; ++k; }
             p = S.pid[i][p];
         }
     }
@@ -310,8 +311,8 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     for (int c = 0; c < nchk; c += 2) {
         if (!__any_sync(FULL, ok)) break;
         const bool two = c + 1 < nchk;
-        const uint32_t w0 = S.chk[c][ccol];
-        const uint32_t w1 = two ? S.chk[c + 1][ccol] : 0u;
+        const uint32_t w0 = CHK(c, ccol);
+        const uint32_t w1 = two ? CHK(c + 1, ccol) : 0u;
         bool r0 = true, r1 = true, need0 = false, need1 = false;
         uint32_t b0 = 0, n0 = 0, b1 = 0, n1 = 0;
         if (ok) {
@@ -368,9 +369,8 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 // the backward images other than the slice's source, then the same-label images that are
 // not backward neighbours (the only ones injectivity must compare: v in N(w) implies v != w).
 template <int D>
-__device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> &S, int l, bool valid,
+__device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, bool valid,
                                             uint32_t lane) {
-    static_assert(GM_CHK_ROWS >= D - 2, "checks + injectivity images of a level: up to D - 2");
     if (!valid) return;
     const uint32_t chkm = P.bw[l] & ~(1u << S.cs[l][lane]), eqm = P.same_lab[l] & ~P.bw[l];
     const int nchk = __popc(P.bw[l]) - 1;
@@ -378,18 +378,18 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.par_low; --i) {
         const uint32_t w = S.v[i][p];
-        if ((chkm >> i) & 1u) { S.chk[kc][lane] = w; ++kc; }
-        if ((eqm >> i) & 1u) { S.chk[nchk + ke][lane] = w; ++ke; }
+        if ((chkm >> i) & 1u) { CHK(kc, lane) = w; ++kc; }
+        if ((eqm >> i) & 1u) { CHK(nchk + ke, lane) = w; ++ke; }
         p = S.pid[i][p];
     }
 #if GM_CHK_ORDER
     // most selective check first: larger device id = lower degree = fewer neighbours, so more
     // tasks fail early and whole warps leave the probe loop sooner
     for (int a = 1; a < nchk; ++a) {
-        const uint32_t x = S.chk[a][lane];
+        const uint32_t x = CHK(a, lane);
         int b = a - 1;
-        while (b >= 0 && S.chk[b][lane] < x) { S.chk[b + 1][lane] = S.chk[b][lane]; --b; }
-        S.chk[b + 1][lane] = x;
+        while (b >= 0 && CHK(b, lane) < x) { CHK(b + 1, lane) = CHK(b, lane); --b; }
+        CHK(b + 1, lane) = x;
     }
 #endif
 }
@@ -407,7 +407,7 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
 // level l = last-1 is entered (prep_last), not once per task: M[b] when b < l, and the
 // same-label images not adjacent to phi[b] in Q (those need an adjacency test).
 template <int D>
-__device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane,
+__device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, bool valid, uint32_t lane,
                                           uint32_t &words) {
     if (!valid) return;
     const int b = (int)P.last_b;
@@ -420,8 +420,8 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     for (int i = l - 1; i >= (int)P.last_low; --i) {
         const uint32_t w = S.v[i][p];
         if (i == b) mb = w;
-        if ((test >> i) & 1u) { S.lastw[k][lane] = w; ++k; }
-        if ((known >> i) & 1u) { S.lastw[P.last_k + ka][lane] = w; ++ka; }
+        if ((test >> i) & 1u) { LASTW(k, lane) = w; ++k; }
+        if ((known >> i) & 1u) { LASTW(P.last_k + ka, lane) = w; ++ka; }
         if ((gt >> i) & 1u) lb = max(lb, w + 1);
         if ((lt >> i) & 1u) ub = min(ub, w);
         p = S.pid[i][p];
@@ -438,13 +438,13 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
                        (uint32_t)__popc(P.last_same & P.last_adj & ((2u << l) - 1));
         words += 2;
         for (int c = 0; c < k; ++c)
-            if (has_edge(P, mb, P.lab[b], S.lastw[c][lane], lab, words)) --cnt;
+            if (has_edge(P, mb, P.lab[b], LASTW(c, lane), lab, words)) --cnt;
         S.lastlb[lane] = cnt;
     }
 }
 
 template <int D>
-__device__ __forceinline__ uint32_t count_last(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t v,
+__device__ __forceinline__ uint32_t count_last(const SearchParams &P, const WarpStack<D> &S, uint32_t *__restrict__ scr, int l, uint32_t v,
                                                uint32_t src, uint32_t &words) {
     const uint32_t lab = P.lab[l + 1];
     const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
@@ -473,11 +473,11 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
             (((P.last_adj >> l) & 1u) || has_edge(P, mb, lb_lab, v, lab, words)))
             --cnt;
         for (uint32_t c = 0; c < P.last_k; ++c) {
-            const uint32_t w = S.lastw[c][src];
+            const uint32_t w = LASTW(c, src);
             if (w >= lb && w < ub && has_edge(P, mb, lb_lab, w, lab, words)) --cnt;
         }
         for (uint32_t c = 0; c < P.last_ka; ++c) {
-            const uint32_t w = S.lastw[P.last_k + c][src];
+            const uint32_t w = LASTW(P.last_k + c, src);
             if (w >= lb && w < ub) --cnt;
         }
         return cnt;
@@ -486,7 +486,7 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     uint32_t cnt = hi - lo - (uint32_t)__popc(same & P.last_adj & ((2u << l) - 1));
     if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lb_lab, v, lab, words)) --cnt;
     for (uint32_t c = 0; c < P.last_k; ++c)
-        if (has_edge(P, mb, lb_lab, S.lastw[c][src], lab, words)) --cnt;
+        if (has_edge(P, mb, lb_lab, LASTW(c, src), lab, words)) --cnt;
     return cnt;
 }
 
@@ -495,9 +495,8 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
 // mapped same-label images (levels < l) inside A, inside R and inside both.  The images'
 // membership is only summed here when no per-task row needs them (!P.two_walk).
 template <int D>
-__device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S, int l, bool valid, uint32_t lane,
+__device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, bool valid, uint32_t lane,
                                          uint32_t &words) {
-    static_assert(GM_LASTW_ROWS >= 6, "prep_two keeps six per-parent words in lastw");
     if (!valid) return;
     const uint32_t lab6 = P.lab[l + 1], lab7 = P.lab[l + 2];
     const int b6 = (int)P.two_b6, b7 = (int)P.two_b7;
@@ -509,16 +508,16 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
         if (i == b7) m7 = w;
         p = S.pid[i][p];
     }
-    S.lastw[0][lane] = m6;
-    S.lastw[1][lane] = m7;
+    LASTW(0, lane) = m6;
+    LASTW(1, lane) = m7;
     if (b6 < l) {
         const uint32_t ra = m6 * P.S + lab6;
-        S.lastw[2][lane] = ld_nc(P.offs + ra); S.lastw[3][lane] = ld_nc(P.offs + ra + 1);
+        LASTW(2, lane) = ld_nc(P.offs + ra); LASTW(3, lane) = ld_nc(P.offs + ra + 1);
         words += 2;
     }
     if (b7 < l) {
         const uint32_t rr = m7 * P.S + lab7;
-        S.lastw[4][lane] = ld_nc(P.offs + rr); S.lastw[5][lane] = ld_nc(P.offs + rr + 1);
+        LASTW(4, lane) = ld_nc(P.offs + rr); LASTW(5, lane) = ld_nc(P.offs + rr + 1);
         words += 2;
     }
     uint32_t inA = 0, inR = 0, inAR = 0;
@@ -552,7 +551,7 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
 // bitmap or by binary search).  Warp-collective: every lane calls it; F = lane has a valid
 // partial match ending in (l, v, src).
 template <int D>
-__device__ __forceinline__ unsigned long long count_two(const SearchParams &P, WarpStack<D> &S, int l,
+__device__ __forceinline__ unsigned long long count_two(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
                                                         uint32_t v, uint32_t src, bool F, uint32_t lane,
                                                         uint32_t &words) {
     const uint32_t lab6 = P.lab[l + 1], lab7 = P.lab[l + 2];
@@ -561,9 +560,9 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
     if (F) {
         // parent-constant parts from prep_two (lastw rows 0-5, lastmb/lb/ub); the row of a
         // backward neighbour mapped at this level (b == l, i.e. v) is read per task
-        if (b6 < l) { m6 = S.lastw[0][src]; a0 = S.lastw[2][src]; a1 = S.lastw[3][src]; }
+        if (b6 < l) { m6 = LASTW(0, src); a0 = LASTW(2, src); a1 = LASTW(3, src); }
         else { const uint32_t ra = v * P.S + lab6; a0 = ld_nc(P.offs + ra); a1 = ld_nc(P.offs + ra + 1); words += 2; }
-        if (b7 < l) { m7 = S.lastw[1][src]; r0 = S.lastw[4][src]; r1 = S.lastw[5][src]; }
+        if (b7 < l) { m7 = LASTW(1, src); r0 = LASTW(4, src); r1 = LASTW(5, src); }
         else { const uint32_t rr = v * P.S + lab7; r0 = ld_nc(P.offs + rr); r1 = ld_nc(P.offs + rr + 1); words += 2; }
         // mapped vertices inside A and R: only same-label ones can be; surely if their query
         // vertex is adjacent to phi[b] in Q, else one edge test
@@ -694,7 +693,9 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 template <int D, bool ENUM>
 __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    WarpStack<D> &S = reinterpret_cast<WarpStack<D> *>(smem_raw)[threadIdx.x >> 5];
+    uint8_t *wbase = smem_raw + (size_t)(threadIdx.x >> 5) * P.warp_stride;
+    WarpStack<D> &S = *reinterpret_cast<WarpStack<D> *>(wbase);
+    uint32_t *__restrict__ scr = reinterpret_cast<uint32_t *>(wbase + sizeof(WarpStack<D>));
     const uint32_t lane = threadIdx.x & 31;
     const int last = (int)P.nq - 1;
     Ctrl *C = P.ctrl;
@@ -757,9 +758,9 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
-                if (d0 == (int)P.par_level) prep_checks<D>(P, S, d0, valid, lane);
-                if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, d0, valid, lane, wacc);
-                if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, d0, valid, lane, wacc);
+                if (d0 == (int)P.par_level) prep_checks<D>(P, S, scr, d0, valid, lane);
+                if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, scr, d0, valid, lane, wacc);
+                if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
                 base = d0; l = d0;
                 got = true;
                 break;
@@ -778,9 +779,9 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
                     __threadfence();
                     ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                 }
-                if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, depth, lane == 0, lane);
-                if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, depth, lane == 0, lane, wacc);
-                if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, depth, lane == 0, lane, wacc);
+                if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, scr, depth, lane == 0, lane);
+                if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
+                if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 base = (int)depth; l = (int)depth;
                 got = true;
                 break;
@@ -917,7 +918,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
 #endif
 
             // ---- Process
-            const bool F = process<D>(P, S, l, v, src, has, lane, l == (int)P.par_level, wacc);
+            const bool F = process<D>(P, S, scr, l, v, src, has, lane, l == (int)P.par_level, wacc);
 #ifdef GM_LEVEL_STATS
             if (lane == 0) atomicAdd(&g_level_pass[l], (unsigned long long)__popc(__ballot_sync(FULL, F)));
             else __ballot_sync(FULL, F);
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
             wacc = 0;
             if (!ENUM && P.bulk_two && l == last - 2) {
                 // pair counting: both remaining levels of every partial match at once
-                my_count += count_two<D>(P, S, l, v, src, F, lane, wacc);
+                my_count += count_two<D>(P, S, scr, l, v, src, F, lane, wacc);
                 __syncwarp();
                 continue;
             }
@@ -956,7 +957,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
             if (!ENUM && P.bulk_last && l == last - 1) {
                 // last-level set counting: the extensions of this partial match are exactly the
                 // label-L(phi[last]) neighbours of its backward neighbour minus the mapped ones
-                if (F) my_count += count_last<D>(P, S, l, v, src, wacc);
+                if (F) my_count += count_last<D>(P, S, scr, l, v, src, wacc);
                 __syncwarp();
                 continue;
             }
@@ -966,9 +967,9 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
             if (!fm) continue;
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
             generate<D>(P, S, l + 1, F, lane, wacc);
-            if (l + 1 == (int)P.par_level) prep_checks<D>(P, S, l + 1, F, lane);
-            if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, l + 1, F, lane, wacc);
-            if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, l + 1, F, lane, wacc);
+            if (l + 1 == (int)P.par_level) prep_checks<D>(P, S, scr, l + 1, F, lane);
+            if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, scr, l + 1, F, lane, wacc);
+            if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, scr, l + 1, F, lane, wacc);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
             __syncwarp();
             ++l;
@@ -1172,7 +1173,8 @@ static size_t stack_bytes() { return sizeof(WarpStack<D>); }
 template <int D, bool ENUM>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
-    const size_t smem = stack_bytes<D>() * wpb;
+    P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last));
+    const size_t smem = (size_t)P.warp_stride * wpb;
     auto kern = k_dfs<D, ENUM>;
     GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int fit = 0;
@@ -1527,6 +1529,21 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 const uint32_t need = (p->bw[l] | P.same_lab[l]) & ((1u << l) - 1);
                 P.par_low = need ? (uint32_t)__builtin_ctz(need) : l;
             }
+        }
+        {   // scratch rows: the most check images any task (or a par-level parent) holds, and the
+            // set / pair counting words
+            const uint32_t last = p->nq - 1;
+            uint32_t rc = 0;
+            for (uint32_t l = 1; l <= last; ++l) rc = std::max<uint32_t>(rc, (uint32_t)__builtin_popcount(p->bw[l]) - 1);
+            if (P.par_level != ~0u && P.par_level >= 1) {   // (level 0 is never entered by the DFS)
+                const uint32_t l = P.par_level;
+                rc = std::max<uint32_t>(rc, (uint32_t)__builtin_popcount(p->bw[l]) - 1 +
+                                                (uint32_t)__builtin_popcount(P.same_lab[l] & ~p->bw[l] & ((1u << l) - 1)));
+            }
+            uint32_t rl = P.bulk_last ? P.last_k + P.last_ka : 0u;
+            if (P.bulk_two) rl = std::max<uint32_t>(rl, 6u);
+            P.rows_chk = rc;
+            P.rows_last = rl;
         }
         GM_CK(cudaEventRecord(d0e, st));
         const uint32_t nq = p->nq;
