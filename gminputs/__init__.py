@@ -202,7 +202,7 @@ def random_query(offs, nbrs, labels, size: int, seed: int, **kw) -> Query:
 
 
 def grow_query(adj, labels, size: int, seed: int, max_restarts: int = 1000,
-               dense: bool = False, min_avg_degree: float = 0.0) -> Query:
+               dense: bool = False, min_avg_degree: float = 0.0, with_vertices: bool = False):
     """§6.1 procedure: random seed vertex, repeatedly add a uniformly random vertex
     adjacent to the current set, keep ALL edges among chosen vertices (induced).
     `adj` provides .n and .neighbors(v) (sorted, simple graph): HostAdjacency or the
@@ -211,7 +211,8 @@ def grow_query(adj, labels, size: int, seed: int, max_restarts: int = 1000,
     dense=True draws the next vertex uniformly among the frontier vertices with the MOST
     neighbours in the chosen set (on sparse power-law graphs the plain procedure almost
     always returns trees; Appendix A's "dense" class needs d_avg >= 3).  Restarts until
-    the query's average degree reaches min_avg_degree."""
+    the query's average degree reaches min_avg_degree.  with_vertices=True also returns the
+    data vertices the query was grown from (query vertex i = chosen[i]: one embedding)."""
     n = adj.n
     ctr = 0
     for _ in range(max_restarts):
@@ -247,7 +248,8 @@ def grow_query(adj, labels, size: int, seed: int, max_restarts: int = 1000,
                         edges.append((idx[v], idx[w]))
             if 2.0 * len(edges) / size < min_avg_degree:
                 continue
-            return Query(size, edges, [int(labels[v]) for v in chosen], name=f"rq{size}_s{seed}")
+            q = Query(size, edges, [int(labels[v]) for v in chosen], name=f"rq{size}_s{seed}")
+            return (q, chosen) if with_vertices else q
     raise RuntimeError("random_query: could not grow a connected query (isolated region)")
 
 

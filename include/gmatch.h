@@ -213,7 +213,15 @@ typedef struct {
                                  bitmaps: candidate reads + row-offset pairs + binary-search
                                  probes + bitmap words (algorithmic bytes = 4 * words) */
     uint64_t automorphisms;   /* |Aut(Q)| the count was scaled by (1: no symmetry breaking) */
+    uint32_t paths;           /* GM_PATH_* bits: the exact shortcuts this call's DFS used */
+    uint32_t stack_levels;    /* levels D of the k_dfs stack instantiation (8, 16 or 32); 0: no DFS */
 } gm_run_stats;
+
+/* gm_run_stats.paths */
+#define GM_PATH_SET_COUNT   1u  /* last level set-counted (count_last) */
+#define GM_PATH_PAIR_COUNT  2u  /* last two levels pair-counted (count_two) */
+#define GM_PATH_PAR_CHECKS  4u  /* per-parent check lists at the hot level (prep_checks) */
+#define GM_PATH_SYMMETRY    8u  /* symmetry-breaking conditions enforced (count x |Aut(Q)|) */
 
 /*
  * gm_count -- count all embeddings of the plan's Q in G (this rank's share).

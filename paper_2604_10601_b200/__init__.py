@@ -241,8 +241,11 @@ def gm_count(p: Plan, out=None, stream=None, **kw):
     o, keep = _opts(**kw)
     st = L.RunStats()
     if out is not None:
+        import torch
         if not _is_torch_cuda(out):
             raise TypeError("out must be a CUDA tensor")
+        if out.dtype not in (torch.int64, torch.uint64) or out.numel() < 1 or not out.is_contiguous():
+            raise TypeError("out must be a contiguous int64/uint64 CUDA tensor with at least 1 element")
         rc = L.lib().gm_count(p._h, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), L.GM_MEM_DEVICE,
                               ctypes.byref(st), _stream_handle(stream))
         L.check(rc, allow=(GM_TIMEOUT,))
@@ -262,8 +265,12 @@ def gm_enumerate(p: Plan, capacity: int, out=None, stream=None, **kw):
     st = L.RunStats()
     c = ctypes.c_uint64(0)
     if out is not None:
+        import torch
         if not _is_torch_cuda(out):
             raise TypeError("out must be a CUDA tensor")
+        if (out.dtype not in (torch.int32, torch.uint32) or not out.is_contiguous()
+                or out.numel() < int(capacity) * p.nq):
+            raise TypeError("out must be a contiguous int32/uint32 CUDA tensor of at least capacity * nq elements")
         rc = L.lib().gm_enumerate(p._h, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), int(capacity),
                                   L.GM_MEM_DEVICE, ctypes.byref(c), ctypes.byref(st), _stream_handle(stream))
         L.check(rc, allow=(GM_TIMEOUT,))

@@ -21,6 +21,7 @@ GM_MAX_QUERY = 32
 GM_FLAG_NO_SET_COUNT = 1
 GM_FLAG_NO_SYMMETRY = 2
 GM_FLAG_NO_PAIR_COUNT = 4
+GM_PATH_SET_COUNT, GM_PATH_PAIR_COUNT, GM_PATH_PAR_CHECKS, GM_PATH_SYMMETRY = 1, 2, 4, 8
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 
 # every symbol include/gmatch.h declares (checked by tests/test_abi.py)
@@ -60,7 +61,8 @@ class RunStats(ctypes.Structure):
                 ("donations", ctypes.c_uint64), ("tasks", ctypes.c_uint64), ("rounds", ctypes.c_uint64),
                 ("dfs_ms", ctypes.c_float), ("total_ms", ctypes.c_float), ("dfs_launches", ctypes.c_uint32),
                 ("kernel_launches", ctypes.c_uint32), ("grid", ctypes.c_uint32), ("block", ctypes.c_uint32),
-                ("words", ctypes.c_uint64), ("automorphisms", ctypes.c_uint64)]
+                ("words", ctypes.c_uint64), ("automorphisms", ctypes.c_uint64), ("paths", ctypes.c_uint32),
+                ("stack_levels", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -191,6 +191,14 @@ __device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t a, uint
     return contains(P.nbr, ld_nc(P.offs + row), ld_nc(P.offs + row + 1), x, words);
 }
 
+// acc += x, recording a wrap past 2^64 - 1 in ovf (per-task counts reach |V| * B in pair
+// counting, so a lane's running sum can wrap long before the final atomicAdd)
+__device__ __forceinline__ void add_count(unsigned long long &acc, unsigned long long x, bool &ovf) {
+    const unsigned long long s = acc + x;
+    ovf |= s < acc;
+    acc = s;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -702,6 +710,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
     volatile Ctrl *VC = C;
 
     unsigned long long my_count = 0, my_tasks = 0, my_rounds = 0, my_don = 0, my_words = 0;
+    bool ovf = false;          // my_count wrapped (add_count)
     uint32_t wacc = 0;
     uint32_t tick = 0;
     bool stop = false;
@@ -927,7 +936,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
             wacc = 0;
             if (!ENUM && P.bulk_two && l == last - 2) {
                 // pair counting: both remaining levels of every partial match at once
-                my_count += count_two<D>(P, S, scr, l, v, src, F, lane, wacc);
+                add_count(my_count, count_two<D>(P, S, scr, l, v, src, F, lane, wacc), ovf);
                 __syncwarp();
                 continue;
             }
@@ -957,7 +966,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
             if (!ENUM && P.bulk_last && l == last - 1) {
                 // last-level set counting: the extensions of this partial match are exactly the
                 // label-L(phi[last]) neighbours of its backward neighbour minus the mapped ones
-                if (F) my_count += count_last<D>(P, S, scr, l, v, src, wacc);
+                if (F) add_count(my_count, count_last<D>(P, S, scr, l, v, src, wacc), ovf);
                 __syncwarp();
                 continue;
             }
@@ -980,11 +989,13 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
     my_words += wacc;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        my_count += __shfl_xor_sync(FULL, my_count, o);
+        add_count(my_count, __shfl_xor_sync(FULL, my_count, o), ovf);
         my_tasks += __shfl_xor_sync(FULL, my_tasks, o);
         my_words += __shfl_xor_sync(FULL, my_words, o);
     }
+    ovf = __any_sync(FULL, ovf);
     if (lane == 0) {
+        if (ovf) atomicExch(&C->overflow, 1);
         if (my_count) {
             const unsigned long long old = atomicAdd(&C->count, my_count);
             if (old + my_count < old) atomicExch(&C->overflow, 1);
@@ -1545,6 +1556,10 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             P.rows_chk = rc;
             P.rows_last = rl;
         }
+        rs.paths = (P.bulk_last ? GM_PATH_SET_COUNT : 0u) | (P.bulk_two ? GM_PATH_PAIR_COUNT : 0u) |
+                   (P.par_level != ~0u && P.par_level >= d ? GM_PATH_PAR_CHECKS : 0u) |
+                   (use_sb ? GM_PATH_SYMMETRY : 0u);
+        rs.stack_levels = p->nq <= 8 ? 8u : (p->nq <= 16 ? 16u : 32u);
         GM_CK(cudaEventRecord(d0e, st));
         const uint32_t nq = p->nq;
         if (nq <= 8)

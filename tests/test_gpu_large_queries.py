@@ -1,0 +1,225 @@
+"""GPU parity for 9-32-vertex queries: the D=16 and D=32 instantiations of k_dfs.
+
+The bench's configs 4 and 5 run 16-, 24- and 32-vertex dense queries (BASELINE.json
+configs[3..4]; the paper evaluates 8-, 12- and 16-vertex random queries, PAPER.md:883,
+and Definition 1, does not get easier with |V(Q)|).  These tests
+compare gm_count and gm_enumerate with the oracle on graphs where the oracle finishes in
+seconds, for every counting path the library has:
+
+  * dense queries grown by the §6.1 procedure with the dense rule of
+    gminputs.grow_query -- many backward neighbours per level, i.e. many adjacency checks
+    per task, and (16 labels over 24-32 query vertices) same-label injectivity rows at
+    levels >= 16;
+  * the same dense cores with one or two pendant leaves, so set counting (one leaf) and
+    pair counting (two non-adjacent leaves, same or different labels) run at D=16/32;
+
+each under default options, set_count=False, pair_count=False and symmetry=False, with
+tau in {1, 64, 1e6} and stealing on and off.  Small results are also enumerated and the
+sorted embedding set compared element by element.
+"""
+import numpy as np
+import pytest
+
+import gminputs as gi
+from oracle import OracleGraph
+
+pytestmark = pytest.mark.gpu
+
+GRAPH = dict(scale=12, ef=8, labels=16, seed=7)     # R-MAT 12 (4096 vertices), 16 uniform labels
+ENUM_MAX = 200_000                                   # enumerate and compare sets up to this many rows
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2604_10601_b200 as gm
+    n, s, d = gi.rmat_edges(GRAPH["scale"], GRAPH["ef"], GRAPH["seed"])
+    lab = gi.uniform_labels(n, GRAPH["labels"], GRAPH["seed"])
+    og = OracleGraph(n, s, d, lab)
+    adj = gi.HostAdjacency(*gi.simple_adjacency(n, s, d))
+    g = gm.gm_load_graph(n, s, d, lab, GRAPH["labels"])
+    return dict(gm=gm, n=n, lab=lab, og=og, adj=adj, g=g, ref={})
+
+
+def with_leaves(core, k_leaves, same, seed):
+    """core + k_leaves pendant vertices (leaf i hangs off core vertex a or b).  Leaves are never
+    adjacent to each other; `same` gives the two leaves one label (pair counting's
+    intersection term)."""
+    rs = np.random.default_rng(seed)
+    n = core.n
+    edges = core.edges.tolist()
+    labels = core.labels.tolist()
+    a = int(rs.integers(0, n))
+    b = a if seed % 2 == 0 else int(rs.integers(0, n))
+    la = int(rs.integers(0, GRAPH["labels"]))
+    for i, p in enumerate([a, b][:k_leaves]):
+        edges.append((p, n + i))
+        labels.append(la if (same or i == 0) else int(rs.integers(0, GRAPH["labels"])))
+    return gi.Query(n + k_leaves, edges, labels, name=f"{core.name}+{k_leaves}l{'s' if same else ''}")
+
+
+# (core size, seed, leaves, same-label leaves); every case verified to finish in the oracle in
+# a few seconds (R-MAT 12, 16 labels).  Sizes 10..32 cover k_dfs<16> (9-16) and k_dfs<32> (17-32).
+DENSE = [(10, 1), (10, 3), (12, 1), (12, 3), (16, 1), (16, 3), (24, 1), (24, 3), (32, 1), (32, 2), (32, 3)]
+LEAVES = [(k, s, nl, same) for k in (10, 14, 22, 30) for s in (1, 3, 4) for nl, same in ((1, False), (2, False), (2, True))
+          if not (k == 14 and s == 4 and same)]
+
+
+def query(env, core_size, seed, leaves=0, same=False):
+    core = gi.grow_query(env["adj"], env["lab"], core_size, seed=seed, dense=True, min_avg_degree=3.0)
+    return with_leaves(core, leaves, same, seed) if leaves else core
+
+
+def oracle_count(env, q):
+    key = (q.n, tuple(map(tuple, q.edges.tolist())), tuple(q.labels.tolist()))
+    if key not in env["ref"]:
+        env["ref"][key] = env["og"].count(q)
+    return env["ref"][key]
+
+
+def sorted_rows(a):
+    a = np.asarray(a, dtype=np.uint32)
+    return a[np.lexsort(a.T[::-1])] if len(a) else a
+
+
+def check_all_paths(env, q, order=None, expect_paths=0):
+    gm = env["gm"]
+    ref = oracle_count(env, q)
+    assert ref > 0                                  # the query was grown from G: at least the identity
+    p = gm.gm_plan_query(env["g"], q, order=order)
+    seen = 0
+    for tau in (1, 64, 10 ** 6):
+        for steal in (True, False):
+            c, st = gm.gm_count(p, tau=tau, steal=steal)
+            assert c == ref, (q.name, tau, steal, st)
+            if st["dfs_launches"]:
+                assert st["stack_levels"] == (16 if q.n <= 16 else 32)
+            seen |= st["paths"]
+    for kw in (dict(set_count=False), dict(pair_count=False), dict(symmetry=False),
+               dict(set_count=False, symmetry=False)):
+        for tau in (1, 64):
+            c, st = gm.gm_count(p, tau=tau, **kw)
+            assert c == ref, (q.name, kw, tau, st)
+            seen |= st["paths"]
+    assert seen & expect_paths == expect_paths, (q.name, seen)
+    if ref <= ENUM_MAX:
+        want = env["og"].enumerate(q)
+        for tau in (1, 10 ** 6):
+            rows, total, _ = gm.gm_enumerate(p, capacity=ref + 3, tau=tau)
+            assert total == ref
+            assert np.array_equal(sorted_rows(rows), want), q.name
+    return ref, seen
+
+
+@pytest.mark.parametrize("k,seed", DENSE)
+def test_dense_query_counts_and_sets(env, k, seed):
+    """Dense grown queries of 10-32 vertices (many checks per task, same-label injectivity rows
+    at high levels) on every counting path, tau and stealing setting."""
+    q = query(env, k, seed)
+    check_all_paths(env, q)
+
+
+@pytest.mark.parametrize("k,seed,leaves,same", LEAVES)
+def test_dense_core_with_leaves(env, k, seed, leaves, same):
+    """Dense cores plus one or two pendant leaves, in the planner's order and with the leaves
+    placed last (set counting with one leaf, pair counting with two) at D=16/32."""
+    from paper_2604_10601_b200 import _lib as L
+    q = query(env, k, seed, leaves, same)
+    check_all_paths(env, q)
+    # leaves last in a connected order of the core (BFS from vertex 0 of the core)
+    core_n = q.n - leaves
+    adjq = {u: set() for u in range(q.n)}
+    for a, b in q.edges.tolist():
+        adjq[a].add(b); adjq[b].add(a)
+    order, seen = [0], {0}
+    i = 0
+    while i < len(order):
+        for w in sorted(adjq[order[i]]):
+            if w < core_n and w not in seen:
+                seen.add(w); order.append(w)
+        i += 1
+    order += list(range(core_n, q.n))
+    expect = L.GM_PATH_SET_COUNT | (L.GM_PATH_PAIR_COUNT if leaves == 2 else 0)
+    check_all_paths(env, q, order=order, expect_paths=expect)
+
+
+def test_stealing_happens_at_d16_and_d32(env):
+    """With a one-item pool (tau = 1) the only way to keep the GPU busy is stealing: donations
+    happen in both the 16- and the 32-level stack, and the counts stay exact."""
+    gm = env["gm"]
+    for k, seed in ((14, 3), (30, 2)):
+        q = query(env, k, seed, 2, False)
+        ref = oracle_count(env, q)
+        p = gm.gm_plan_query(env["g"], q)
+        don = 0
+        for kw in (dict(), dict(set_count=False, symmetry=False), dict(pair_count=False)):
+            c, st = gm.gm_count(p, tau=1, steal=True, **kw)
+            assert c == ref, (q.name, kw)
+            don += st["donations"]
+        assert don > 0, q.name
+
+
+def test_root_restricted_counts_large(env):
+    """User root lists (no symmetry breaking) at D=16/32: the count over sampled roots equals the
+    oracle's per-root counts summed."""
+    gm = env["gm"]
+    og = env["og"]
+    rs = np.random.default_rng(5)
+    for k, seed, leaves in ((12, 1, 0), (22, 3, 2), (30, 4, 1)):
+        q = query(env, k, seed, leaves)
+        p = gm.gm_plan_query(env["g"], q)
+        u0 = p.info()["order"][0]
+        cands = np.flatnonzero(p.candidates(u0))
+        roots = rs.permutation(cands)[:24]
+        ref = sum(og.count(q, fixed=(u0, int(v))) for v in roots)
+        for tau in (1, 10 ** 6):
+            assert gm.gm_count(p, roots=roots.astype(np.uint32), tau=tau)[0] == ref
+
+
+def test_config4_sampled_roots_full_queries():
+    """configs[3] at full size: R-MAT scale 24 (16.8 M vertices, ~265 M adjacency entries, 16
+    labels) with the bench's own 16-vertex dense queries, counted by k_dfs<16, false> in the
+    bench's launch configuration (tau = 1e6, stealing on) restricted to sampled roots of
+    phi[0], equal the oracle's per-root counts on the whole graph (roots whose oracle search
+    stays under a node budget; the query's own seed image is tried first, so nonzero counts
+    are covered)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import bench
+    import gminputs.gpu as gg
+    import paper_2604_10601_b200 as gm
+    cfg = bench.CONFIGS["rmat24"]
+    n, s, d, lab = bench.make_graph_device(cfg)
+    lh = lab.cpu().numpy().view(np.uint32)
+    adj = gg.DeviceNeighbors(n, s, d)
+    queries = bench.build_queries(cfg, adj, lh)
+    seeds = [gi.grow_query(adj, lh, q.n, seed=sd, dense=True, min_avg_degree=3.0, with_vertices=True)[1]
+             for q, sd in zip(queries, cfg["dense"])]
+    g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
+    og = OracleGraph(n, s.cpu().numpy().view(np.uint32), d.cpu().numpy().view(np.uint32), lh)
+    del adj, s, d
+    torch.cuda.empty_cache()
+    rs = np.random.default_rng(24)
+    checked = nonzero = 0
+    for q, chosen in zip(queries, seeds):
+        p = gm.gm_plan_query(g, q)
+        u0 = p.info()["order"][0]
+        cands = np.flatnonzero(p.candidates(u0))
+        roots, ref = [], 0
+        for v in [int(chosen[u0])] + [int(x) for x in rs.permutation(cands)[:200]]:
+            if v in roots:
+                continue
+            c = og.count(q, fixed=(u0, v), max_nodes=2_000_000)
+            if c is not None:
+                roots.append(v); ref += c; nonzero += c > 0
+                assert gm.gm_count(p, roots=np.array([v], np.uint32), time_limit_ms=60000)[0] == c, (q.name, v)
+            if len(roots) == 6:
+                break
+        c, st = gm.gm_count(p, roots=np.array(roots, np.uint32), time_limit_ms=60000)
+        assert st["timed_out"] == 0 and st["stack_levels"] == 16
+        assert c == ref, (q.name, roots)
+        checked += len(roots)
+    assert checked >= 12 and nonzero >= 1, (checked, nonzero)
