@@ -84,6 +84,16 @@ def build_queries(cfg, adj, lab):
     return qs
 
 
+def build_complete_queries(cfg, adj, lab):
+    """The config's complete-run query set (no time limit binds: query ms is a latency)."""
+    import gminputs as gi
+    c = cfg.get("complete")
+    if not c:
+        return []
+    qs = [gi.grow_query(adj, lab, k, seed=sd, dense=True, min_avg_degree=3.0) for k, sd in zip(c["sizes"], c["seeds"])]
+    return qs
+
+
 def make_graph_host(cfg):
     import gminputs as gi
     if cfg["kind"] == "rmat":
@@ -193,15 +203,18 @@ def run_reference(args, cfg, world, rank):
         "config": {"workload": args.config, "desc": cfg["desc"]},
         "cpu_baseline": {"value": value, "unit": "embeddings/s", "cores": 1, "kind": "oracle",
                          "sample": f"per step: embeddings found by the oracle rooted at "
-                                   f"{int(np.mean(samples))} random roots (query vertex 0 pinned, <= 2e6 "
-                                   f"search-tree nodes per root) across {len(qs)} queries, "
+                                   f"{int(np.mean(samples))} random roots (query vertex 0 pinned, <= "
+                                   f"{ORACLE_MAX_NODES:.0e} search-tree nodes per root) across {len(qs)} queries, "
                                    f"~{budget_s:.0f}s of one host core"},
         "e2e": {"value": value, "unit": "embeddings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def oracle_sample(og, qs, lab, rs, budget_s, max_nodes=200_000):
+ORACLE_MAX_NODES = 200_000     # search-tree nodes per sampled root (both oracle legs)
+
+
+def oracle_sample(og, qs, lab, rs, budget_s, max_nodes=ORACLE_MAX_NODES):
     """The oracle on bounded work, like the GPU arm's time-limited queries: for each query,
     random roots for query vertex 0, each searched for at most max_nodes tree nodes, until
     budget_s/len(qs) seconds of one core are spent.  Returns (embeddings found, seconds,
@@ -228,11 +241,33 @@ def cpu_baseline(cfg, qs, n, s, d, lab, budget_s=12.0):
     c, dt, nroots = oracle_sample(og, qs, lab, np.random.default_rng(0), budget_s)
     return {"value": c / dt, "unit": "embeddings/s", "cores": 1, "kind": "oracle",
             "sample": f"embeddings found by the oracle rooted at {nroots} random roots (query vertex 0 "
-                      f"pinned, <= 2e5 search-tree nodes per root) across the {len(qs)} queries of this "
+                      f"pinned, <= {ORACLE_MAX_NODES:.0e} search-tree nodes per root) across the {len(qs)} queries of this "
                       f"workload, {dt:.1f}s of one host core"}
 
 
 # ----------------------------------------------------------------------------- our arm
+
+# The paper's own numbers, quoted with the GPU it names (context only, not a target): Table 2
+# (PAPER.md:626-666), gMatch (GM) search time in ms on an RTX 4090 (PAPER.md:579, 128 SMs, 24 GB),
+# unlabelled small patterns P1-P9 (Figure 8, an image: the patterns are not defined in the text);
+# lj is LiveJournal (config 4's shape), fr is Friendster (config 5's shape).
+PAPER_CONTEXT = {
+    "gpu": "NVIDIA RTX 4090 (PAPER.md:579)",
+    "source": "PAPER.md Table 2 (lines 626-666), gMatch column, search time ms",
+    "lj_ms": {"P1": 31, "P2": 422, "P3": 2080, "P4": 4127, "P5": 334373, "P6": 637667, "P7": 305968,
+              "P8": 221493, "P9": 25114},
+    "fr_ms": {"P1": 4354, "P2": 12132, "P3": 53556, "P4": 2806445, "P5": 1068031, "P6": 1519540,
+              "P7": 731884, "P8": 235798, "P9": 33776},
+    "idle_rate": "< 5 % on 12-vertex queries (PAPER.md:744, Table 5)",
+}
+
+
+def idle_rate(tasks, rounds):
+    """Idle lane-slots of the DFS's scatter rounds: 1 - tasks / (32 * rounds).  The batched
+    analogue of the paper's idle rate (the mean over partial matches of
+    (32 - |C_M^L(u)|) / 32): the share of lanes a round leaves without a task."""
+    return 1.0 - tasks / (32.0 * rounds) if rounds else None
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -244,13 +279,19 @@ def main():
     ap.add_argument("--time-limit-ms", type=float, default=None)
     ap.add_argument("--tau", type=float, default=1e6)
     ap.add_argument("--no-steal", action="store_true")
+    ap.add_argument("--root-order", default="shuffled", choices=["shuffled", "hubs"],
+                    help="pool order of the timed steps: seeded root permutation (default: a time-limited "
+                         "query explores a uniform sample of its roots) or device-id order (hubs first)")
     ap.add_argument("--static-roots", action="store_true",
                     help="N > 1: static (v/64) %% N root partition instead of the shared pool counter")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--per-query", action="store_true", help="print per-query timings to stderr")
+    ap.add_argument("--no-context", action="store_true", help="skip the context legs (hubs-first order, "
+                    "Alg. 2 as written, gm_enumerate, the complete query set)")
+    ap.add_argument("--per-query", action="store_true", help="also print the per-query list to stderr")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     limit = cfg["limit_ms"] if args.time_limit_ms is None else args.time_limit_ms
+    root_seed = 1 if args.root_order == "shuffled" else 0
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -288,68 +329,127 @@ def main():
         import gminputs.gpu as gg
         adj = gg.DeviceNeighbors(n, s_dev, d_dev)
     qs = build_queries(cfg, adj, lab_h)
+    cq = build_complete_queries(cfg, adj, lab_h) if not args.no_context else []
     del adj
     g = gm.gm_load_graph(n, s_dev, d_dev, lab_dev, cfg["labels"])
     del s_dev, d_dev
     torch.cuda.empty_cache()
     ginfo = g.info()
     stream = torch.cuda.current_stream()
-    run_kw = dict(tau=int(args.tau), rank=rank, world=world, steal=not args.no_steal, time_limit_ms=limit)
-    # N > 1: dynamic chunk assignment -- every rank's DFS claims pool batches from ONE counter
-    # in rank 0's memory (CUDA IPC + NVLink peer atomics); --static-roots: (v/64) % N partition
+    run_kw = dict(tau=int(args.tau), rank=rank, world=world, steal=not args.no_steal, time_limit_ms=limit,
+                  root_seed=root_seed)
+    # N > 1: dynamic chunk assignment -- every rank's DFS claims pool batches from counters in
+    # rank 0's memory (CUDA IPC + NVLink peer atomics, one slot per query, reset once per
+    # step); --static-roots: (v/64) % N partition
     shared_ptr = None
+    nslots = max(len(qs), len(cq), 1)
     if world > 1 and not args.static_roots:
         if rank == 0:
-            shared_ptr, handle = gm.gm_pool_counter_create()
+            shared_ptr, handle = gm.gm_pool_counter_create(nslots)
         box = [handle if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         if rank != 0:
             shared_ptr = gm.gm_pool_counter_open(box[0])
-        run_kw = dict(tau=int(args.tau), steal=not args.no_steal, time_limit_ms=limit, shared_pool_ctr=shared_ptr)
+        run_kw = dict(tau=int(args.tau), steal=not args.no_steal, time_limit_ms=limit, root_seed=root_seed)
 
-    counts_dev = torch.zeros(len(qs), dtype=torch.int64, device=dev)
+    counts_dev = torch.zeros(nslots, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    def step(record):
-        """One pass of the hot path over the query set; returns per-query (stats, plan_ms)."""
+    def reset_slots():
+        """Shared pool counters: zeroed by rank 0 before a step; every rank waits (outside the
+        timed region) so no rank claims from a slot before its reset."""
+        if shared_ptr is not None:
+            if rank == 0:
+                gm.gm_pool_counter_reset(shared_ptr, nslots)
+            torch.cuda.synchronize()
+            dist.barrier()
+
+    def step(queries, kw_extra=None):
+        """One pass of the hot path over a query set: per query gm_plan_query (filter + order)
+        and gm_count (BFS pool + DFS).  Returns per-query (stats, start event, end event) and
+        the reduced count halves (the step's one collective for N > 1)."""
         out = []
-        plans = []
-        for i, q in enumerate(qs):
+        for i, q in enumerate(queries):
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             p = gm.gm_plan_query(g, q, filter="nlf")
-            if shared_ptr is not None:          # reset the shared counter, then start together
-                if rank == 0:
-                    gm.gm_pool_counter_reset(shared_ptr)
-                torch.cuda.synchronize()
-                dist.barrier()
-            _, st = gm.gm_count(p, out=counts_dev[i:i + 1], **run_kw)
-            if shared_ptr is not None:
-                dist.barrier()                  # nobody resets while another rank still searches
+            kw = dict(run_kw, **(kw_extra or {}))
+            if shared_ptr is not None:          # query i claims from its own slot (reset per step)
+                kw["shared_pool_ctr"] = gm.pool_counter_slot(shared_ptr, i)
+            _, st = gm.gm_count(p, out=counts_dev[i:i + 1], **kw)
             e1.record(stream)
-            plans.append(p)
             out.append((st, e0, e1))
-        halves = partition.reduce_count_halves(counts_dev)   # the one collective of the step (N > 1)
-        return out, plans, halves
+            del p
+        halves = partition.reduce_count_halves(counts_dev[:len(queries)])
+        return out, halves
+
+    def rank_sums(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t)
+        return t.tolist()
+
+    def rank_max(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def summarize(queries, res, exact):
+        """Per-query list (exact counts summed over ranks; work counters summed; times max over
+        ranks)."""
+        loc = []
+        for st, e0, e1 in res:
+            loc += [st["tasks"], st["rounds"], st["words"], st["donations"], st["timed_out"]]
+        sums = rank_sums(loc)
+        tmax = rank_max([e0.elapsed_time(e1) for _, e0, e1 in res] + [st["dfs_ms"] for st, _, _ in res])
+        nq = len(queries)
+        rows = []
+        for i, (q, (st, _, _)) in enumerate(zip(queries, res)):
+            tasks, rounds, words, don, to = sums[5 * i:5 * i + 5]
+            rows.append({"q": q.name, "n": int(q.n), "m": int(len(q.edges)), "embeddings": exact[i],
+                         "completed": to == 0, "ms": round(tmax[i], 3), "dfs_ms": round(tmax[nq + i], 3),
+                         "tasks": int(tasks), "rounds": int(rounds), "words": int(words),
+                         "idle_rate": None if not rounds else round(idle_rate(tasks, rounds), 4),
+                         "aut": st["automorphisms"], "paths": st["paths"], "D": st["stack_levels"],
+                         "pool": st["pool_size"], "depth": st["pool_depth"], "donations": int(don)})
+        return rows
+
+    def one_pass(queries, kw_extra=None):
+        """Untimed-by-contract context leg: one flushed pass, device-timed per query."""
+        flush.zero_()
+        reset_slots()
+        torch.cuda.synchronize()
+        res, halves = step(queries, kw_extra)
+        torch.cuda.synchronize()
+        exact = partition.count_totals(halves)
+        rows = summarize(queries, res, exact)
+        t = sum(r["ms"] for r in rows)
+        return {"value": sum(exact) / (t / 1e3) if t else None, "unit": "embeddings/s",
+                "ms": round(t, 3), "tasks_per_s": sum(r["tasks"] for r in rows) / (t / 1e3) if t else None,
+                "solved": sum(r["completed"] for r in rows), "queries": len(rows), "per_query": rows}
 
     for _ in range(args.warmup):
         flush.zero_()
-        step(False)
+        reset_slots()
+        step(qs)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(gpu)
     clocks.start()
     step_ms, dfs_ms, dfs_launches, words, kernel_launches = [], [], 0, 0, 0
-    total_emb, q_ms, timeouts, tasks = 0, [], 0, 0
-    per_query = []
+    total_emb, timeouts, tasks, rounds = 0, 0, 0, 0
+    q_ms_all, q_ms_solved = [], []
+    per_query = None
     for k in range(args.steps):
         flush.zero_()                                # L2 flush outside the timed region
+        reset_slots()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        res, plans, halves = step(True)
+        res, halves = step(qs)
         s1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -357,54 +457,47 @@ def main():
         step_ms.append(s0.elapsed_time(s1))
         exact = partition.count_totals(halves)       # exact uint64 sums (no int64 wrap)
         total_emb += sum(exact)
-        for i, (st, e0, e1) in enumerate(res):
-            q_ms.append(e0.elapsed_time(e1))
+        for st, e0, e1 in res:
             dfs_ms.append(st["dfs_ms"])
             dfs_launches += st["dfs_launches"]
             words += st["words"]
             tasks += st["tasks"]
+            rounds += st["rounds"]
             kernel_launches += st["kernel_launches"] + 1       # + the filter kernel of the plan
             timeouts += st["timed_out"]
-            if k == 0:
-                per_query.append({"q": qs[i].name, "m": int(len(qs[i].edges)), "ms": round(q_ms[-1], 3),
-                                  "embeddings": exact[i], "aut": st["automorphisms"],
-                                  "dfs_ms": round(st["dfs_ms"], 3), "timed_out": st["timed_out"],
-                                  "pool": st["pool_size"], "depth": st["pool_depth"],
-                                  "donations": st["donations"]})
-        del plans
+        rows = summarize(qs, res, exact)             # (collectives outside the timed region)
+        for r in rows:
+            q_ms_all.append(r["ms"])
+            if r["completed"]:
+                q_ms_solved.append(r["ms"])
+        if per_query is None:
+            per_query = rows
     clk = clocks.stop()
 
     # ---- max over ranks
-    t_local = torch.tensor([sum(step_ms), sum(dfs_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    T_ms, T_dfs = float(t_local[0]), float(t_local[1])
-    w_local = torch.tensor([words, tasks, kernel_launches], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(w_local)
-    words_all, tasks_all, launches_all = (float(x) for x in w_local)
+    T_ms, T_dfs = rank_max([sum(step_ms), sum(dfs_ms)])
+    words_all, tasks_all, rounds_all, launches_all, timeouts_all = rank_sums(
+        [words, tasks, rounds, kernel_launches, timeouts])
     emb_per_step = total_emb / args.steps
     value = total_emb / (T_ms / 1e3)
 
     # ---- end to end through the public API with host buffers (rank-local share, wall clock)
     e2e_emb, e2e_s, h2d, d2h = 0, 0.0, 0, 0
-    for k in range(max(1, args.steps)):
+    e2e_steps = max(1, min(args.steps, 5))
+    for k in range(e2e_steps):
         flush.zero_()
+        reset_slots()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         local = []
-        for q in qs:
+        for i, q in enumerate(qs):
             p = gm.gm_plan_query(g, q, filter="nlf")      # query arrays copied H2D by the library
+            kw = dict(run_kw)
             if shared_ptr is not None:
-                if rank == 0:
-                    gm.gm_pool_counter_reset(shared_ptr)
-                torch.cuda.synchronize()
-                dist.barrier()
-            c, _ = gm.gm_count(p, **run_kw)                # count read back D2H
-            if shared_ptr is not None:
-                dist.barrier()
+                kw["shared_pool_ctr"] = gm.pool_counter_slot(shared_ptr, i)
+            c, _ = gm.gm_count(p, **kw)                    # count read back D2H
             local.append(c)
             h2d += q.edges.nbytes + q.labels.nbytes
             d2h += 8
@@ -413,14 +506,61 @@ def main():
             local = partition.reduce_counts(t)
             d2h += 8 * len(qs)
         dt = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+        dt = rank_max([dt])[0]
         e2e_s += dt
         e2e_emb += sum(local)
-    e2e = {"value": e2e_emb / e2e_s, "unit": "embeddings/s", "h2d_bytes_per_step": h2d // max(1, args.steps),
-           "d2h_bytes_per_step": d2h // max(1, args.steps)}
+    e2e = {"value": e2e_emb / e2e_s, "unit": "embeddings/s", "h2d_bytes_per_step": h2d // e2e_steps,
+           "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps}
+    if s_h is not None:
+        # gm_load_graph from host (pinned) edge arrays: the transfer + CSR build a user pays once
+        # per graph (PAPER.md:681 counts t_transfer in t_query), reported beside e2e
+        sp = torch.from_numpy(s_h.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        dp = torch.from_numpy(d_h.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        lp = torch.from_numpy(lab_h.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g2 = gm.gm_load_graph(n, sp, dp, lp, cfg["labels"])
+        torch.cuda.synchronize()
+        e2e["graph_load_ms"] = round(1e3 * (time.perf_counter() - t0), 3)
+        e2e["graph_load_h2d_bytes"] = int(sp.nbytes + dp.nbytes + lp.nbytes)
+        g2.free()
+        del g2
+
+    # ---- context legs (one flushed pass each, device-timed; not the headline)
+    context = None
+    if not args.no_context:
+        context = {
+            "root_order_of_headline": args.root_order,
+            "hubs_first": one_pass(qs, dict(root_seed=0)) if root_seed else one_pass(qs, dict(root_seed=1)),
+            "alg2_as_written": one_pass(qs, dict(set_count=False, pair_count=False)),
+            "complete_set": one_pass(cq, dict(time_limit_ms=cfg.get("complete_limit_ms", 60000.0))) if cq else None,
+            "paper": PAPER_CONTEXT,
+        }
+        if not args.root_order == "shuffled":
+            context["shuffled"] = context.pop("hubs_first")
+        context["alg2_as_written"]["note"] = ("set counting and pair counting off: every last-level "
+                                              "candidate validated as its own task (Alg. 2 lines 12-13)")
+        if context["complete_set"]:
+            context["complete_set"]["desc"] = cfg.get("complete_desc")
+        # gm_enumerate: embeddings written to a device buffer (rows of nq uint32), same limit
+        enum = []
+        cap = cfg.get("enum_capacity", 1 << 22)
+        for q in qs:
+            p = gm.gm_plan_query(g, q, filter="nlf")
+            buf = torch.empty(cap * q.n, dtype=torch.int32, device=dev)
+            flush.zero_()
+            torch.cuda.synchronize()
+            _, tot, st = gm.gm_enumerate(p, cap, out=buf, time_limit_ms=limit, root_seed=root_seed,
+                                         tau=int(args.tau), rank=rank, world=world)
+            enum.append((q.name, tot, min(tot, cap), st["total_ms"], st["timed_out"]))
+            del buf, p
+        tms = sum(e[3] for e in enum)
+        context["enumerate"] = {"value": sum(e[1] for e in enum) / (tms / 1e3), "unit": "embeddings/s",
+                                "rows_written_per_s": sum(e[2] for e in enum) / (tms / 1e3),
+                                "capacity_rows_per_query": cap,
+                                "per_query": [{"q": a, "embeddings": b, "rows": c, "ms": round(d, 3),
+                                               "timed_out": e} for a, b, c, d, e in enum],
+                                "note": "gm_enumerate to a device buffer, rank-local (not reduced)"}
 
     if rank != 0:
         if world > 1:
@@ -432,12 +572,15 @@ def main():
     dfs_launch_ms = T_dfs / max(1, dfs_launches) if dfs_launches else None
     bytes_per_launch = 4.0 * words_all / max(1, dfs_launches * (world if world > 1 else 1)) if dfs_launches else 0
     achieved = (4.0 * words_all / world) / (T_dfs / 1e3) / 1e9 if T_dfs > 0 else 0.0
-    traffic = None
+    traffic, ncu = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(args.config)
+            tj = json.load(f)
+        traffic = tj.get(args.config)
+        ncu = tj.get("ncu", {}).get(args.config)
     except Exception:
         pass
+    solved = len(q_ms_solved)
     line = {
         "metric": "embeddings/sec", "value": value, "unit": "embeddings/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -446,26 +589,36 @@ def main():
         # per-GPU work (a time budget) is fixed as N grows
         "scaling": "weak" if limit > 0 else "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "queries": len(qs),
-                   "query_ms_mean": statistics.mean(q_ms), "query_ms_median": statistics.median(q_ms),
-                   "per_query_time_limit_ms": limit, "timed_out_queries_per_step": timeouts / args.steps,
+                   "per_query_time_limit_ms": limit,
+                   "root_order": ("seeded pseudo-random root permutation (root_seed=1): a time-limited query "
+                                  "counts the embeddings of a uniform sample of its roots"
+                                  if root_seed else "device-id order (hubs first)"),
+                   "solved_queries_per_step": solved / args.steps,
+                   "unsolved_queries_per_step": (len(q_ms_all) - solved) / args.steps,
+                   "query_ms_mean": statistics.mean(q_ms_all),
+                   "query_ms_mean_solved": statistics.mean(q_ms_solved) if q_ms_solved else None,
                    "embeddings_per_step": emb_per_step, "tau": int(args.tau), "steal": not args.no_steal,
-                   "filter": "nlf", "graph": {k: ginfo[k] for k in ("n", "num_adj", "num_labels", "d_max")},
+                   "filter": "nlf", "graph": {k: ginfo[k] for k in ("n", "num_adj", "num_labels", "d_max", "hubs")},
                    "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": ("1 GPU, whole pool on one device" if world == 1 else
                                    f"{world} GPU(s), CSR replicated, " +
-                                   ("pool batches claimed from one shared counter (NVLink peer atomics)"
+                                   ("pool batches claimed from shared counters (NVLink peer system-scope atomics)"
                                     if shared_ptr is not None else "static root partition") +
                                    ", 1 all-reduce of the counts per step")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_dfs", "launch_ms_mean": dfs_launch_ms,
                      "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_kind,
-                     "share_of_step": T_dfs / T_ms if T_ms else None},
+                     "share_of_step": T_dfs / T_ms if T_ms else None, "ncu": ncu},
         "gpu_launches": int(launches_all),
         "tasks_per_s": tasks_all / (T_ms / 1e3),
+        "idle_rate": idle_rate(tasks_all, rounds_all),
         "clocks": clk,
         "e2e": e2e,
+        "per_query": per_query,
     }
+    if context is not None:
+        line["context"] = context
     if not args.no_cpu_baseline and world == 1:
         if s_h is not None:
             line["cpu_baseline"] = cpu_baseline(cfg, qs, n, s_h, d_h, lab_h)

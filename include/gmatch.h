@@ -191,6 +191,12 @@ typedef struct {
                                 initial pool (rank/world are ignored) and their DFS kernels
                                 claim pool batches from this one counter -- dynamic chunk
                                 assignment across GPUs through NVLink peer atomics */
+    uint64_t root_seed;      /* 0: root candidates in device-id order (degree-descending: hubs
+                                first, the heaviest subtrees claimed first); else a seeded
+                                pseudo-random permutation of them, so a time-limited run
+                                explores a uniform sample of the roots (the BFS pool keeps the
+                                root order).  Counts of completed runs never depend on it; ranks
+                                sharing a pool counter must pass the same seed. */
 } gm_run_opts;
 
 GM_API void gm_default_opts(gm_run_opts *o);
@@ -243,26 +249,36 @@ GM_API int gm_count(const gm_plan *p, const gm_run_opts *opts, uint64_t *count_o
 GM_API int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t *out, uint64_t capacity,
                  int mem, uint64_t *count_host, gm_run_stats *stats, void *stream);
 
-/* ------------------------------------------------------------------ multi-GPU pool counter */
+/* ------------------------------------------------------------------ multi-GPU pool counters */
 
 /*
- * A 64-bit counter in one GPU's memory that the DFS kernels of several ranks (processes, one
- * per GPU) atomically claim pool batches from, over NVLink peer memory -- the north_star's
- * "root-level candidates ... partitioned across the 8 GPUs with dynamic chunk assignment".
- *   gm_pool_counter_create: allocate it on the current device (zeroed); copies a
- *       GM_IPC_HANDLE_BYTES CUDA IPC handle into ipc_handle_out for the other ranks.
- *   gm_pool_counter_open:   map another process's counter (any GPU of the node, or the
- *       same GPU) into this process; *counter_dev is then usable as shared_pool_ctr.
- *   gm_pool_counter_reset:  set it to 0 on `stream` (call on one rank before each search).
+ * An array of 64-bit counters in one GPU's memory that the DFS kernels of several ranks
+ * (processes, one per GPU) atomically claim pool batches from, over NVLink peer memory -- the
+ * north_star's "root-level candidates ... partitioned across the 8 GPUs with dynamic chunk
+ * assignment" (§4.3, 445: warps fetch from the pool with an atomic counter;
+ * the inter-block mechanism is "replicated at the block level using global memory").
+ * Slot k lives at (char *)counter_dev + k * GM_POOL_COUNTER_STRIDE (its own 128-byte line),
+ * so a step of several queries gives each query its own slot and resets them all once.
+ *   gm_pool_counter_create: allocate `slots` counters on the current device (zeroed); copies
+ *       a GM_IPC_HANDLE_BYTES CUDA IPC handle into ipc_handle_out for the other ranks.
+ *       slots in [1, 2^20], else GM_ERR_ARG.
+ *   gm_pool_counter_open:   map another process's counters (any GPU of the node, or the same
+ *       GPU) into this process; *counter_dev (+ k * stride) is then usable as shared_pool_ctr.
+ *   gm_pool_counter_reset:  zero the first `slots` counters on `stream` (one rank).
  *   gm_pool_counter_close:  owner = 1 frees the allocation, owner = 0 unmaps it.
- * Protocol: reset on one rank, synchronize all ranks (barrier), run gm_count on every rank
- * with the same plan inputs and shared_pool_ctr set, synchronize again before the next reset;
- * sum the per-rank counts (one all-reduce).
+ * Memory model: the DFS claims with system-scope atomics (atomicAdd_system) and polls with
+ * relaxed system-scope loads whenever shared_pool_ctr is set: a device-scope atomic is only
+ * atomic among the threads of one GPU.
+ * Protocol per step: reset all slots on one rank and synchronize that stream, barrier, then
+ * every rank runs gm_count for query i with shared_pool_ctr = slot i and the same plan
+ * inputs (no barrier between queries: slots are independent); sum the per-rank counts (one
+ * all-reduce).  A slot must not be reset while a rank may still claim from it.
  */
 #define GM_IPC_HANDLE_BYTES 64
-GM_API int gm_pool_counter_create(void **counter_dev, void *ipc_handle_out);
+#define GM_POOL_COUNTER_STRIDE 128
+GM_API int gm_pool_counter_create(uint32_t slots, void **counter_dev, void *ipc_handle_out);
 GM_API int gm_pool_counter_open(const void *ipc_handle, void **counter_dev);
-GM_API int gm_pool_counter_reset(void *counter_dev, void *stream);
+GM_API int gm_pool_counter_reset(void *counter_dev, uint32_t slots, void *stream);
 GM_API int gm_pool_counter_close(void *counter_dev, int owner);
 
 /* Thread-local description of the last error (empty string if none). */

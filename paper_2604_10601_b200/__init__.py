@@ -178,7 +178,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
           time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True, pair_count=True,
-          shared_pool_ctr=None):
+          shared_pool_ctr=None, root_seed=0):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -208,27 +208,33 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.flags |= L.GM_FLAG_NO_SYMMETRY
     if shared_pool_ctr is not None:
         o.shared_pool_ctr = ctypes.c_void_p(int(shared_pool_ctr))
+    o.root_seed = int(root_seed)
     return o, keep
 
 
-def gm_pool_counter_create():
-    """(device pointer, IPC handle bytes) of a new cross-rank pool counter on this GPU."""
+def gm_pool_counter_create(slots: int = 1):
+    """(device pointer, IPC handle bytes) of `slots` new cross-rank pool counters on this GPU."""
     ptr = ctypes.c_void_p(0)
     h = (ctypes.c_char * L.GM_IPC_HANDLE_BYTES)()
-    L.check(L.lib().gm_pool_counter_create(ctypes.byref(ptr), h))
+    L.check(L.lib().gm_pool_counter_create(int(slots), ctypes.byref(ptr), h))
     return ptr.value, bytes(h)
 
 
 def gm_pool_counter_open(handle: bytes):
-    """Map another rank's pool counter; returns its device pointer in this process."""
+    """Map another rank's pool counters; returns their base device pointer in this process."""
     ptr = ctypes.c_void_p(0)
     buf = (ctypes.c_char * L.GM_IPC_HANDLE_BYTES).from_buffer_copy(handle)
     L.check(L.lib().gm_pool_counter_open(buf, ctypes.byref(ptr)))
     return ptr.value
 
 
-def gm_pool_counter_reset(ptr, stream=None):
-    L.check(L.lib().gm_pool_counter_reset(ctypes.c_void_p(ptr), _stream_handle(stream)))
+def pool_counter_slot(ptr, k: int):
+    """Device pointer of counter slot k (gmatch.h: base + k * GM_POOL_COUNTER_STRIDE)."""
+    return int(ptr) + int(k) * L.GM_POOL_COUNTER_STRIDE
+
+
+def gm_pool_counter_reset(ptr, slots: int = 1, stream=None):
+    L.check(L.lib().gm_pool_counter_reset(ctypes.c_void_p(ptr), int(slots), _stream_handle(stream)))
 
 
 def gm_pool_counter_close(ptr, owner: bool):

@@ -32,6 +32,7 @@ EXPORTS = [
     "gm_pool_counter_create", "gm_pool_counter_open", "gm_pool_counter_reset", "gm_pool_counter_close",
 ]
 GM_IPC_HANDLE_BYTES = 64
+GM_POOL_COUNTER_STRIDE = 128
 
 
 class GraphInfo(ctypes.Structure):
@@ -52,7 +53,7 @@ class RunOpts(ctypes.Structure):
                 ("blocks_per_sm", ctypes.c_uint32), ("warps_per_block", ctypes.c_uint32),
                 ("time_limit_ms", ctypes.c_double), ("roots", ctypes.POINTER(ctypes.c_uint32)),
                 ("num_roots", ctypes.c_uint64), ("pool_bytes_max", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("shared_pool_ctr", ctypes.c_void_p)]
+                ("flags", ctypes.c_uint32), ("shared_pool_ctr", ctypes.c_void_p), ("root_seed", ctypes.c_uint64)]
 
 
 class RunStats(ctypes.Structure):
@@ -98,9 +99,9 @@ def lib():
         L.gm_count.argtypes = [vp, ctypes.POINTER(RunOpts), vp, ctypes.c_int, ctypes.POINTER(RunStats), vp]
         L.gm_enumerate.argtypes = [vp, ctypes.POINTER(RunOpts), vp, ctypes.c_uint64, ctypes.c_int, u64p,
                                    ctypes.POINTER(RunStats), vp]
-        L.gm_pool_counter_create.argtypes = [ctypes.POINTER(vp), vp]
+        L.gm_pool_counter_create.argtypes = [ctypes.c_uint32, ctypes.POINTER(vp), vp]
         L.gm_pool_counter_open.argtypes = [vp, ctypes.POINTER(vp)]
-        L.gm_pool_counter_reset.argtypes = [vp, vp]
+        L.gm_pool_counter_reset.argtypes = [vp, ctypes.c_uint32, vp]
         L.gm_pool_counter_close.argtypes = [vp, ctypes.c_int]
         L.gm_last_error.restype = ctypes.c_char_p
         L.gm_version.restype = ctypes.c_char_p

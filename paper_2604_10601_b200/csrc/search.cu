@@ -53,8 +53,11 @@ constexpr uint32_t FULL = 0xffffffffu;
 #define GM_VHUB 1
 #endif
 #ifndef GM_DFS_MINB
-#define GM_DFS_MINB 9
+#define GM_DFS_MINB 9      // resident 128-thread blocks per SM for the 8-level kernel (<= 56 registers)
 #endif
+// 16/32-level kernels: the WarpStack (7.8 / 15.6 KB per warp) limits residency to ~6 / ~3 blocks
+// per SM, so they may use the registers that frees
+#define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? 6 : 3))
 constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
 constexpr uint32_t kItemWords = 4 + kMaxQ;     // [depth, cb, cl, cs, prefix[kMaxQ]]
 
@@ -102,6 +105,7 @@ struct SearchParams {
     Ctrl *ctrl;
     uint32_t batch;             // pool items fetched per warp (<= 32)
     unsigned long long *pool_ctr;  // &ctrl->pool_ctr, or a counter shared across ranks
+    uint32_t pool_sys;          // 1: pool_ctr is shared by several GPUs (system-scope atomics)
     uint32_t *q_items;          // q_cap * kItemWords
     unsigned long long *q_seq;  // q_cap per-slot sequence numbers (Vyukov bounded MPMC ring)
     unsigned long long q_cap;
@@ -197,6 +201,20 @@ __device__ __forceinline__ void add_count(unsigned long long &acc, unsigned long
     const unsigned long long s = acc + x;
     ovf |= s < acc;
     acc = s;
+}
+
+// The pool counter.  Shared by several GPUs (peer memory over NVLink, gm_pool_counter_*), a
+// device-scope atomic is atomic only among the threads of ONE GPU (PTX memory model), so the
+// claim is a system-scope atomicAdd and the poll a relaxed system-scope load; the pool items
+// themselves are per-GPU replicas, so no ordering beyond the counter's own atomicity is needed.
+__device__ __forceinline__ unsigned long long pool_peek(const SearchParams &P) {
+    unsigned long long x;
+    if (P.pool_sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(P.pool_ctr) : "memory");
+    else x = *(volatile unsigned long long *)P.pool_ctr;
+    return x;
+}
+__device__ __forceinline__ unsigned long long pool_claim(const SearchParams &P, unsigned long long n) {
+    return P.pool_sys ? atomicAdd_system(P.pool_ctr, n) : atomicAdd(P.pool_ctr, n);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -313,60 +331,57 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         }
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
-    // Two checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
-    // independent, so each lane keeps two dependent-load chains in flight (ncu: the kernel
-    // is bound by long-scoreboard stalls on L2-resident probes, not by bandwidth).
-    for (int c = 0; c < nchk; c += 2) {
+    // G checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
+    // independent, so each lane keeps G dependent-load chains in flight (ncu: the kernel is
+    // bound by long-scoreboard stalls on its probes, not by bandwidth).  G = 2 for the
+    // L2-resident small-query kernel (issue-bound: fewer wasted probes), 4 for the 16/32-level
+    // kernels that run the DRAM-resident configs (more memory-level parallelism per warp).
+    constexpr int G = D <= 8 ? 2 : 4;
+    for (int c = 0; c < nchk; c += G) {
         if (!__any_sync(FULL, ok)) break;
-        const bool two = c + 1 < nchk;
-        const uint32_t w0 = CHK(c, ccol);
-        const uint32_t w1 = two ? CHK(c + 1, ccol) : 0u;
-        bool r0 = true, r1 = true, need0 = false, need1 = false;
-        uint32_t b0 = 0, n0 = 0, b1 = 0, n1 = 0;
-        if (ok) {
-            // hub bitmap of w, or of v (the test is symmetric), else binary search of w's row
-            if (w0 < P.nhubs || (GM_VHUB && v < P.nhubs)) {
-                const uint32_t h = w0 < P.nhubs ? w0 : v, x = w0 < P.nhubs ? v : w0;
-                r0 = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
-                ++words;
-            } else {
-                const uint32_t row = w0 * P.S + lab;
-                b0 = ld_nc(P.offs + row);
-                n0 = ld_nc(P.offs + row + 1) - b0;
-                need0 = true;
-                words += 2;
-            }
-            if (two) {
-                if (w1 < P.nhubs || (GM_VHUB && v < P.nhubs)) {
-                    const uint32_t h = w1 < P.nhubs ? w1 : v, x = w1 < P.nhubs ? v : w1;
-                    r1 = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+        uint32_t w[G], b[G], n[G];
+        bool r[G], need[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const bool act = ok && c + g < nchk;
+            w[g] = act ? CHK(c + g, ccol) : 0u;
+            r[g] = true; need[g] = false; b[g] = 0; n[g] = 0;
+            if (act) {
+                // hub bitmap of w, or of v (the test is symmetric), else binary search of w's row
+                if (w[g] < P.nhubs || (GM_VHUB && v < P.nhubs)) {
+                    const uint32_t h = w[g] < P.nhubs ? w[g] : v, x = w[g] < P.nhubs ? v : w[g];
+                    r[g] = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
                     ++words;
                 } else {
-                    const uint32_t row = w1 * P.S + lab;
-                    b1 = ld_nc(P.offs + row);
-                    n1 = ld_nc(P.offs + row + 1) - b1;
-                    need1 = true;
+                    const uint32_t row = w[g] * P.S + lab;
+                    b[g] = ld_nc(P.offs + row);
+                    n[g] = ld_nc(P.offs + row + 1) - b[g];
+                    need[g] = true;
                     words += 2;
                 }
             }
         }
-        while (__any_sync(FULL, n0 > 1 || n1 > 1)) {   // lock-step branch-free lower bounds
-            if (n0 > 1) {
-                const uint32_t half = n0 >> 1;
-                b0 = (ld_nc(P.nbr + b0 + half) <= v) ? b0 + half : b0;
-                n0 -= half;
-                ++words;
-            }
-            if (n1 > 1) {
-                const uint32_t half = n1 >> 1;
-                b1 = (ld_nc(P.nbr + b1 + half) <= v) ? b1 + half : b1;
-                n1 -= half;
-                ++words;
+        bool more = false;
+#pragma unroll
+        for (int g = 0; g < G; ++g) more = more || n[g] > 1;
+        while (__any_sync(FULL, more)) {   // lock-step branch-free lower bounds
+            more = false;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (n[g] > 1) {
+                    const uint32_t half = n[g] >> 1;
+                    b[g] = (ld_nc(P.nbr + b[g] + half) <= v) ? b[g] + half : b[g];
+                    n[g] -= half;
+                    ++words;
+                    more = more || n[g] > 1;
+                }
             }
         }
-        if (need0) { r0 = n0 == 1 && ld_nc(P.nbr + b0) == v; words += n0; }
-        if (need1) { r1 = n1 == 1 && ld_nc(P.nbr + b1) == v; words += n1; }
-        ok = ok && r0 && r1;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (need[g]) { r[g] = n[g] == 1 && ld_nc(P.nbr + b[g]) == v; words += n[g]; }
+            ok = ok && r[g];
+        }
     }
     return ok;
 }
@@ -699,7 +714,7 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // ------------------------------------------------------------------ DFS kernel
 
 template <int D, bool ENUM>
-__global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const SearchParams P) {
+__global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t *wbase = smem_raw + (size_t)(threadIdx.x >> 5) * P.warp_stride;
     WarpStack<D> &S = *reinterpret_cast<WarpStack<D> *>(wbase);
@@ -729,11 +744,11 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
             if (lane == 0) {
                 if (VC->abort) {
                     exit_now = 1;
-                } else if (*(volatile unsigned long long *)P.pool_ctr < P.pool_size) {
+                } else if (pool_peek(P) < P.pool_size) {
                     atomicAdd(&C->work, 1);
                     // P.pool_ctr: this launch's counter, or one shared by every rank's launch
                     // (peer memory over NVLink: multi-GPU dynamic chunk assignment)
-                    b = atomicAdd(P.pool_ctr, (unsigned long long)P.batch);
+                    b = pool_claim(P, (unsigned long long)P.batch);
                     if (b >= P.pool_size) { atomicSub(&C->work, 1); b = ~0ull; }
                 }
                 if (!exit_now && b == ~0ull) {
@@ -745,7 +760,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB) k_dfs(const Se
                         const unsigned long long pos = VC->q_head;
                         const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
                         if (seq == pos + 1 && atomicCAS(&C->q_head, pos, pos + 1) == pos) item = pos;
-                        if (item == ~0ull && *(volatile unsigned long long *)P.pool_ctr >= P.pool_size &&
+                        if (item == ~0ull && pool_peek(P) >= P.pool_size &&
                             VC->work == 0)
                             exit_now = 1;
                     }
@@ -1129,6 +1144,23 @@ struct RootSel {
         return v;
     }
 };
+// Seeded permutation key of a root (splitmix64 finaliser of seed and vertex): sorting the
+// root list by it gives a pseudo-random root order (gm_run_opts.root_seed).
+struct RootKey {
+    const uint32_t *roots;
+    unsigned long long seed;
+    __device__ unsigned long long operator()(unsigned long long i) const {
+        unsigned long long z = seed * 0x9E3779B97F4A7C15ull + roots[i] + 1;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+};
+__global__ void k_root_keys(RootKey rk, unsigned long long n, unsigned long long *keys) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        keys[i] = rk(i);
+}
 struct NotNone {
     __device__ bool operator()(uint32_t x) const { return x != 0xffffffffu; }
 };
@@ -1367,6 +1399,27 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     GM_CK(cudaStreamSynchronize(st));
     if (d_user) { cudaFree(d_user); d_user = nullptr; }
     rs.roots = nroots;
+    if (o.root_seed && nroots > 1) {
+        // seeded root order: sort (key, root) pairs by the key; buf[1] holds keys in/out and
+        // roots out, item_off the keys' sorted copy
+        const size_t kb = sizeof(unsigned long long) * nroots;
+        rc = ensure(W.buf[1], W.buf_bytes[1], 2 * kb + sizeof(uint32_t) * nroots);
+        if (rc) return rc;
+        rc = ensure(W.item_off, W.item_off_bytes, kb);
+        if (rc) return rc;
+        unsigned long long *keys = reinterpret_cast<unsigned long long *>(W.buf[1]);
+        unsigned long long *keys_out = reinterpret_cast<unsigned long long *>(W.item_off);
+        uint32_t *roots_out = reinterpret_cast<uint32_t *>(keys + nroots);
+        k_root_keys<<<grid_for(nroots, 256, W.sms), 256, 0, st>>>(RootKey{W.buf[0], o.root_seed}, nroots, keys);
+        GM_CK(cudaGetLastError());
+        size_t tb = 0;
+        GM_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_out, W.buf[0], roots_out, (int64_t)nroots, 0, 64, st));
+        rc = ensure(W.tmp, W.tmp_bytes, tb + 16);
+        if (rc) return rc;
+        GM_CK(cub::DeviceRadixSort::SortPairs(W.tmp, tb, keys, keys_out, W.buf[0], roots_out, (int64_t)nroots, 0, 64, st));
+        GM_CK(cudaMemcpyAsync(W.buf[0], roots_out, sizeof(uint32_t) * nroots, cudaMemcpyDeviceToDevice, st));
+        launches += 2;
+    }
 
     uint32_t *frontier = W.buf[0];
     int cur = 0;
@@ -1473,6 +1526,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.pool = frontier;
         P.pool_ctr = o.shared_pool_ctr ? reinterpret_cast<unsigned long long *>(o.shared_pool_ctr)
                                        : &W.ctrl->pool_ctr;
+        P.pool_sys = o.shared_pool_ctr ? 1u : 0u;
         P.pool_size = P_n;
         P.d0 = d;
         P.steal = o.steal ? 1 : 0;
@@ -1640,13 +1694,15 @@ extern "C" int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t 
 
 // ------------------------------------------------------------------ multi-GPU pool counter
 
-extern "C" int gm_pool_counter_create(void **counter_dev, void *ipc_handle_out) {
+extern "C" int gm_pool_counter_create(uint32_t slots, void **counter_dev, void *ipc_handle_out) {
     set_error("");
     GM_REQ(counter_dev && ipc_handle_out, GM_ERR_ARG, "gm_pool_counter_create: NULL argument");
+    GM_REQ(slots >= 1 && slots <= (1u << 20), GM_ERR_ARG, "gm_pool_counter_create: slots %u outside [1, 2^20]", slots);
     static_assert(sizeof(cudaIpcMemHandle_t) <= GM_IPC_HANDLE_BYTES, "IPC handle size");
     void *p = nullptr;
-    GM_CK(cudaMalloc(&p, 256));                 // own 256-byte block: the counter's line alone
-    GM_CK(cudaMemset(p, 0, 256));
+    const size_t bytes = (size_t)slots * GM_POOL_COUNTER_STRIDE;   // one 128-byte line per slot
+    GM_CK(cudaMalloc(&p, bytes));
+    GM_CK(cudaMemset(p, 0, bytes));
     cudaIpcMemHandle_t h;
     GM_CK(cudaIpcGetMemHandle(&h, p));
     memset(ipc_handle_out, 0, GM_IPC_HANDLE_BYTES);
@@ -1666,9 +1722,11 @@ extern "C" int gm_pool_counter_open(const void *ipc_handle, void **counter_dev) 
     return GM_OK;
 }
 
-extern "C" int gm_pool_counter_reset(void *counter_dev, void *stream) {
+extern "C" int gm_pool_counter_reset(void *counter_dev, uint32_t slots, void *stream) {
+    set_error("");
     GM_REQ(counter_dev, GM_ERR_ARG, "gm_pool_counter_reset: NULL counter");
-    GM_CK(cudaMemsetAsync(counter_dev, 0, sizeof(unsigned long long), (cudaStream_t)stream));
+    GM_REQ(slots >= 1, GM_ERR_ARG, "gm_pool_counter_reset: slots = 0");
+    GM_CK(cudaMemsetAsync(counter_dev, 0, (size_t)slots * GM_POOL_COUNTER_STRIDE, (cudaStream_t)stream));
     return GM_OK;
 }
 

@@ -35,7 +35,7 @@ def _worker(rank, world, port, out):
                    gi.clique(3), gi.cycle(4)]
         # shared pool counter: rank 0 owns it, the others map it through CUDA IPC
         if rank == 0:
-            ptr, handle = gm.gm_pool_counter_create()
+            ptr, handle = gm.gm_pool_counter_create(len(queries))
         else:
             ptr, handle = None, None
         box = [handle]
@@ -44,15 +44,15 @@ def _worker(rank, world, port, out):
             ptr = gm.gm_pool_counter_open(box[0])
         static = torch.zeros(len(queries), dtype=torch.int64)
         shared = torch.zeros(len(queries), dtype=torch.int64)
+        # one counter slot per query, all reset once; no barrier between queries
+        if rank == 0:
+            gm.gm_pool_counter_reset(ptr, len(queries))
+            torch.cuda.synchronize()
+        dist.barrier()
         for i, q in enumerate(queries):
             p = gm.gm_plan_query(g, q)
             static[i] = gm.gm_count(p, rank=rank, world=world, root_chunk=8, tau=64)[0]
-            if rank == 0:
-                gm.gm_pool_counter_reset(ptr)
-                torch.cuda.synchronize()
-            dist.barrier()
-            shared[i] = gm.gm_count(p, shared_pool_ctr=ptr, tau=256)[0]
-            dist.barrier()
+            shared[i] = gm.gm_count(p, shared_pool_ctr=gm.pool_counter_slot(ptr, i), tau=256)[0]
         dist.all_reduce(static)
         dist.all_reduce(shared)
         if rank == 0:
