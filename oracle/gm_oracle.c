@@ -159,6 +159,9 @@ static void search(or_ctx *c, int depth) {
         uint32_t w = c->map[c->first_back[depth]];
         for (int64_t e = c->g->off[w]; e < c->g->off[w + 1]; e++) {
             uint32_t v = c->g->adj[e];
+            /* the budget also counts candidates examined, so a budgeted call is bounded even
+               when every node scans a hub's adjacency (budget only: no effect on results) */
+            if (c->max_nodes && ++c->nodes > c->max_nodes) return;
             if (!feasible(c, depth, v)) continue;
             c->map[u] = v; c->used[v] = 1;
             search(c, depth + 1);
@@ -166,6 +169,7 @@ static void search(or_ctx *c, int depth) {
         }
     } else {
         for (int64_t v = 0; v < c->g->n; v++) {
+            if (c->max_nodes && ++c->nodes > c->max_nodes) return;
             if (!feasible(c, depth, (uint32_t)v)) continue;
             c->map[u] = (uint32_t)v; c->used[v] = 1;
             search(c, depth + 1);
@@ -193,7 +197,8 @@ uint64_t or_count(const or_graph *g, int nq, int mq, const uint32_t *qedges,
 }
 
 /*
- * Same as or_count, with a budget of max_nodes visited search-tree nodes (0 = none).
+ * Same as or_count, with a budget of max_nodes units of search work (0 = none): one unit per
+ * visited search-tree node and per candidate examined.
  * Returns UINT64_MAX - 1 when the budget ran out (the count is then unknown); used only to
  * pick samples the oracle can finish, never to produce a partial expected value.
  */

@@ -57,7 +57,16 @@ constexpr uint32_t FULL = 0xffffffffu;
 #endif
 // 16/32-level kernels: the WarpStack (7.8 / 15.6 KB per warp) limits residency to ~6 / ~3 blocks
 // per SM, so they may use the registers that frees
-#define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? 6 : 3))
+#ifndef GM_MINB16
+#define GM_MINB16 6
+#endif
+#ifndef GM_MINB32
+#define GM_MINB32 3
+#endif
+#define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? GM_MINB16 : GM_MINB32))
+#ifndef GM_PROBES_WIDE
+#define GM_PROBES_WIDE 4   // probes in flight per lane in the 16/32-level kernels (process())
+#endif
 constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
 constexpr uint32_t kItemWords = 4 + kMaxQ;     // [depth, cb, cl, cs, prefix[kMaxQ]]
 
@@ -336,7 +345,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     // bound by long-scoreboard stalls on its probes, not by bandwidth).  G = 2 for the
     // L2-resident small-query kernel (issue-bound: fewer wasted probes), 4 for the 16/32-level
     // kernels that run the DRAM-resident configs (more memory-level parallelism per warp).
-    constexpr int G = D <= 8 ? 2 : 4;
+    constexpr int G = D <= 8 ? 2 : GM_PROBES_WIDE;
     for (int c = 0; c < nchk; c += G) {
         if (!__any_sync(FULL, ok)) break;
         uint32_t w[G], b[G], n[G];

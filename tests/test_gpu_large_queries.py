@@ -191,6 +191,8 @@ def test_config4_sampled_roots_full_queries():
     import bench
     import gminputs.gpu as gg
     import paper_2604_10601_b200 as gm
+    import time
+    t0 = time.time()
     cfg = bench.CONFIGS["rmat24"]
     n, s, d, lab = bench.make_graph_device(cfg)
     lh = lab.cpu().numpy().view(np.uint32)
@@ -199,7 +201,9 @@ def test_config4_sampled_roots_full_queries():
     seeds = [gi.grow_query(adj, lh, q.n, seed=sd, dense=True, min_avg_degree=3.0, with_vertices=True)[1]
              for q, sd in zip(queries, cfg["dense"])]
     g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
+    print(f"[config4] graph + queries {time.time() - t0:.1f}s", flush=True)
     og = OracleGraph(n, s.cpu().numpy().view(np.uint32), d.cpu().numpy().view(np.uint32), lh)
+    print(f"[config4] oracle graph {time.time() - t0:.1f}s", flush=True)
     del adj, s, d
     torch.cuda.empty_cache()
     rs = np.random.default_rng(24)
@@ -209,7 +213,7 @@ def test_config4_sampled_roots_full_queries():
         u0 = p.info()["order"][0]
         cands = np.flatnonzero(p.candidates(u0))
         roots, ref = [], 0
-        for v in [int(chosen[u0])] + [int(x) for x in rs.permutation(cands)[:200]]:
+        for v in [int(chosen[u0])] + [int(x) for x in rs.permutation(cands)[:100]]:
             if v in roots:
                 continue
             c = og.count(q, fixed=(u0, v), max_nodes=2_000_000)
@@ -219,6 +223,7 @@ def test_config4_sampled_roots_full_queries():
             if len(roots) == 6:
                 break
         c, st = gm.gm_count(p, roots=np.array(roots, np.uint32), time_limit_ms=60000)
+        print(f"[config4] {q.name}: {len(roots)} roots, count {ref}, {time.time() - t0:.1f}s", flush=True)
         assert st["timed_out"] == 0 and st["stack_levels"] == 16
         assert c == ref, (q.name, roots)
         checked += len(roots)

@@ -385,7 +385,7 @@ def test_config3_sampled_roots(gm):
         u0 = p.info()["order"][0]
         roots, ref = [], 0
         for v in rs.choice(n, 400, replace=False):
-            c = og.count(q, fixed=(u0, int(v)), max_nodes=200_000)
+            c = og.count(q, fixed=(u0, int(v)), max_nodes=4_000_000)
             if c is not None:
                 roots.append(int(v)); ref += c; nonzero += c > 0
             if len(roots) == 12:
@@ -437,7 +437,7 @@ def test_config2_sampled_roots(gm):
     g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
     og = OracleGraph(n, s, d, lab)
     rs = np.random.default_rng(1)
-    budget = 100_000            # oracle search-tree nodes per sampled root
+    budget = 2_000_000          # oracle work units (tree nodes + candidates examined) per sampled root
     checked, nonzero = 0, 0
     for q in queries:
         p = gm.gm_plan_query(g, q)
@@ -465,7 +465,7 @@ def test_config2_sampled_roots(gm):
         s0 = ps.info()["order"][0]
         sroots, sref = [], 0
         for v in rs.permutation(np.flatnonzero(ps.candidates(s0)))[:100]:
-            cc = og.count(sub, fixed=(s0, int(v)), max_nodes=1_000_000)
+            cc = og.count(sub, fixed=(s0, int(v)), max_nodes=20_000_000)
             if cc is not None:
                 sroots.append(int(v)); sref += cc
                 nonzero += cc > 0

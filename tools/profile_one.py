@@ -23,7 +23,17 @@ if cfg.get("dense") or cfg.get("sparse"):
     adj = gg.DeviceNeighbors(n, s, d)
 else:
     adj = None                      # fixed patterns only
-qs = bench.build_queries(cfg, adj, lh)
+# query growth on scale-24/26 graphs scans the device edge list per vertex: cache the queries
+import hashlib  # noqa: E402
+cache = f"/tmp/gm_queries_{cfgname}_{hashlib.sha1(repr(sorted(cfg.items())).encode()).hexdigest()[:10]}.json"
+if os.path.exists(cache):
+    import json
+    qs = [gi.Query(d_["n"], d_["edges"], d_["labels"], d_["name"]) for d_ in json.load(open(cache))]
+else:
+    qs = bench.build_queries(cfg, adj, lh)
+    import json
+    json.dump([{"n": int(q.n), "edges": q.edges.tolist(), "labels": q.labels.tolist(), "name": q.name} for q in qs],
+              open(cache, "w"))
 g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
 if os.environ.get("GM_HUB_MB"):                 # hub-index sweeps
     g.build_hubs(int(float(os.environ["GM_HUB_MB"]) * (1 << 20)), int(os.environ.get("GM_HUB_MIN", "64")))
