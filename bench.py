@@ -542,25 +542,29 @@ def main():
                                               "candidate validated as its own task (Alg. 2 lines 12-13)")
         if context["complete_set"]:
             context["complete_set"]["desc"] = cfg.get("complete_desc")
-        # gm_enumerate: embeddings written to a device buffer (rows of nq uint32), same limit
+        # gm_enumerate: embeddings written as rows (nq uint32 each, original ids) to a device
+        # buffer of `cap` rows; the search stops when the buffer is full (stop_at_capacity) or
+        # at the time limit, so rows/s is the output rate of the enumerate kernel
         enum = []
-        cap = cfg.get("enum_capacity", 1 << 22)
+        cap = (1 << 26) // max(q.n for q in qs)
         for q in qs:
             p = gm.gm_plan_query(g, q, filter="nlf")
             buf = torch.empty(cap * q.n, dtype=torch.int32, device=dev)
             flush.zero_()
             torch.cuda.synchronize()
             _, tot, st = gm.gm_enumerate(p, cap, out=buf, time_limit_ms=limit, root_seed=root_seed,
-                                         tau=int(args.tau), rank=rank, world=world)
+                                         tau=int(args.tau), rank=rank, world=world, stop_at_capacity=True)
             enum.append((q.name, tot, min(tot, cap), st["total_ms"], st["timed_out"]))
             del buf, p
         tms = sum(e[3] for e in enum)
-        context["enumerate"] = {"value": sum(e[1] for e in enum) / (tms / 1e3), "unit": "embeddings/s",
-                                "rows_written_per_s": sum(e[2] for e in enum) / (tms / 1e3),
+        context["enumerate"] = {"value": sum(e[2] for e in enum) / (tms / 1e3), "unit": "embeddings/s",
+                                "rows_bytes_per_s": sum(e[2] * q.n * 4 for e, q in zip(enum, qs)) / (tms / 1e3),
                                 "capacity_rows_per_query": cap,
-                                "per_query": [{"q": a, "embeddings": b, "rows": c, "ms": round(d, 3),
-                                               "timed_out": e} for a, b, c, d, e in enum],
-                                "note": "gm_enumerate to a device buffer, rank-local (not reduced)"}
+                                "per_query": [{"q": a, "found": b, "rows": c, "ms": round(d, 3),
+                                               "stopped": e} for a, b, c, d, e in enum],
+                                "note": "gm_enumerate writing rows to a device buffer until it is full "
+                                        "(GM_FLAG_STOP_AT_CAPACITY) or the time limit; value = rows written "
+                                        "per second, rank-local"}
 
     if rank != 0:
         if world > 1:

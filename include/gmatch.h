@@ -167,6 +167,9 @@ GM_API void gm_free_plan(gm_plan *p);
 #define GM_FLAG_NO_PAIR_COUNT 4u /* gm_count: do not count the last two levels in bulk when
                                     phi[last-1] and phi[last] are non-adjacent vertices with one
                                     backward neighbour each (pair counting) */
+#define GM_FLAG_STOP_AT_CAPACITY 8u /* gm_enumerate: stop the search once `capacity` rows are
+                                    written (returns GM_TIMEOUT; *count_host is then the number
+                                    found so far, >= capacity) -- for timing row output */
 #define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
                                     Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)|.
                                     Symmetry breaking is also skipped when `roots` is given. */

@@ -178,7 +178,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
           time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True, pair_count=True,
-          shared_pool_ctr=None, root_seed=0):
+          shared_pool_ctr=None, root_seed=0, stop_at_capacity=False):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -206,6 +206,8 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.flags |= L.GM_FLAG_NO_PAIR_COUNT
     if not symmetry:
         o.flags |= L.GM_FLAG_NO_SYMMETRY
+    if stop_at_capacity:
+        o.flags |= L.GM_FLAG_STOP_AT_CAPACITY
     if shared_pool_ctr is not None:
         o.shared_pool_ctr = ctypes.c_void_p(int(shared_pool_ctr))
     o.root_seed = int(root_seed)

@@ -21,6 +21,7 @@ GM_MAX_QUERY = 32
 GM_FLAG_NO_SET_COUNT = 1
 GM_FLAG_NO_SYMMETRY = 2
 GM_FLAG_NO_PAIR_COUNT = 4
+GM_FLAG_STOP_AT_CAPACITY = 8
 GM_PATH_SET_COUNT, GM_PATH_PAIR_COUNT, GM_PATH_PAR_CHECKS, GM_PATH_SYMMETRY = 1, 2, 4, 8
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 

@@ -64,6 +64,9 @@ constexpr uint32_t FULL = 0xffffffffu;
 #define GM_MINB32 3
 #endif
 #define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? GM_MINB16 : GM_MINB32))
+#ifndef GM_TWO_VEC
+#define GM_TWO_VEC 1       // pair-counting intersection: 128-element rounds with 16-byte loads
+#endif
 #ifndef GM_PROBES_WIDE
 #define GM_PROBES_WIDE 4   // probes in flight per lane in the 16/32-level kernels (process())
 #endif
@@ -144,6 +147,7 @@ struct SearchParams {
     uint32_t par_low;           // deepest level prep_checks visits
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
+    uint32_t stop_at_cap;       // enumerate: stop once out_cap rows are written
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
 };
 
@@ -637,6 +641,58 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
             while (true) {
                 // fast path: the cursor's list alone fills the round (long lists against a hub)
                 const uint32_t sl_ci = __shfl_sync(FULL, sl, ci & 31);
+#if GM_TWO_VEC
+                if (ci < 32 && sl_ci - cj >= 128) {
+                    // 128 elements per round with one 16-byte load per lane (LDG.E.128): lane j
+                    // takes the 4 words at a + 4j of the aligned block [a, a + 128) that holds
+                    // the cursor (words before the cursor are masked; a + 128 <= the list's end
+                    // because >= 128 remain), and keeps 4 independent probes in flight.  The
+                    // elements form a set, so the order they are tested in is immaterial.
+                    const uint32_t f_sb = __shfl_sync(FULL, sb, ci), f_gb = __shfl_sync(FULL, gb, ci);
+                    const uint32_t f_ge = __shfl_sync(FULL, ge, ci), f_gown = __shfl_sync(FULL, gown, ci);
+                    const uint32_t start = f_sb + cj, a = start & ~3u;
+                    const uint4 q4 = __ldg(reinterpret_cast<const uint4 *>(P.nbr + a) + lane);
+                    const uint32_t x[4] = {q4.x, q4.y, q4.z, q4.w};
+                    bool hit[4];
+                    uint32_t nval = 0;
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        hit[g] = a + 4 * lane + g >= start;
+                        nval += hit[g];
+                    }
+                    words += nval;
+                    if (f_gown < P.nhubs) {
+                        const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
+                        uint32_t wv[4];
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) wv[g] = hit[g] ? ld_nc(row + (x[g] >> 5)) : 0u;
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) hit[g] = hit[g] && ((wv[g] >> (x[g] & 31)) & 1u);
+                        words += nval;
+                    } else {
+                        // four lower bounds in the same list: the trip count is warp-uniform
+                        uint32_t n = f_ge - f_gb, b[4] = {f_gb, f_gb, f_gb, f_gb};
+                        while (n > 1) {
+                            const uint32_t half = n >> 1;
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) b[g] = (ld_nc(P.nbr + b[g] + half) <= x[g]) ? b[g] + half : b[g];
+                            n -= half;
+                            words += nval;
+                        }
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) hit[g] = hit[g] && n == 1 && ld_nc(P.nbr + b[g]) == x[g];
+                        words += nval;
+                    }
+                    uint32_t h = 0;
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) h += __popc(__ballot_sync(FULL, hit[g]));
+                    if (lane == 0) S.tacc[ci] += h;
+                    __syncwarp();
+                    cj += a + 128 - start;
+                    if (cj == sl_ci) { ++ci; cj = 0; }
+                    continue;
+                }
+#endif
                 if (ci < 32 && sl_ci - cj >= 32) {
                     const uint32_t f_sb = __shfl_sync(FULL, sb, ci), f_gb = __shfl_sync(FULL, gb, ci);
                     const uint32_t f_ge = __shfl_sync(FULL, ge, ci), f_gown = __shfl_sync(FULL, gown, ci);
@@ -968,7 +1024,11 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 if (ENUM) {
                     const uint32_t fm = __ballot_sync(FULL, F);
                     unsigned long long basepos = 0;
-                    if (lane == 0 && fm) basepos = atomicAdd(&C->out_ctr, (unsigned long long)__popc(fm));
+                    if (lane == 0 && fm) {
+                        basepos = atomicAdd(&C->out_ctr, (unsigned long long)__popc(fm));
+                        // GM_FLAG_STOP_AT_CAPACITY: the buffer is full, stop the search
+                        if (P.stop_at_cap && basepos + __popc(fm) >= P.out_cap) atomicExch(&C->abort, 1);
+                    }
                     basepos = __shfl_sync(FULL, basepos, 0);
                     if (F) {
                         const unsigned long long idx = basepos + __popc(fm & ((1u << lane) - 1));
@@ -1540,7 +1600,10 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.d0 = d;
         P.steal = o.steal ? 1 : 0;
         P.q_items = W.q_items; P.q_seq = W.q_seq; P.q_cap = o.steal ? W.q_cap : 1;
-        if (enumerate) { P.out = out_dev(); P.out_cap = cap; }
+        if (enumerate) {
+            P.out = out_dev(); P.out_cap = cap;
+            P.stop_at_cap = (o.flags & GM_FLAG_STOP_AT_CAPACITY) ? 1u : 0u;
+        }
         // the time limit covers the DFS launch (the BFS init phase is short and bounded by tau)
         P.limit_ns = o.time_limit_ms > 0 ? (unsigned long long)(o.time_limit_ms * 1e6) : 0ull;
         {   // last-level set counting applies when phi[last] has exactly one backward neighbour

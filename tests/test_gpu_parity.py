@@ -669,3 +669,53 @@ def test_launch_shape_options(gm):
     with pytest.raises(gm.GMError) as e:
         gm.gm_count(p, warps_per_block=8)
     assert "warps_per_block" in str(e.value)
+
+
+def test_pair_count_long_lists_closed_form(gm):
+    """Pair counting with both leaf lists long (>= 128: the 16-byte-load intersection rounds)
+    on R-MAT 13 unlabelled: 4-vertex paths x-a-b-y in the order [a, b, x, y] (the two leaves
+    hang off different vertices and share a label, so |A n R| is intersected).  The count is
+    pinned by a closed form, not the oracle: ordered walks a-b with x in N(a) \\ {b},
+    y in N(b) \\ {a}, x != y number sum over ordered edges of (d_a - 1)(d_b - 1) - t(a, b),
+    and sum over ordered edges of t(a, b) = |N(a) n N(b)| is trace(A^3)."""
+    import scipy.sparse as sp
+    n, s, d = gi.rmat_edges(13, 16, 77)
+    off, nb = gi.simple_adjacency(n, s, d)
+    deg = np.diff(off).astype(np.int64)
+    rows = np.repeat(np.arange(n), deg)
+    A = sp.csr_matrix((np.ones(len(nb), np.int64), (rows, nb.astype(np.int64))), shape=(n, n))
+    tr3 = int((A @ A).multiply(A).sum())
+    want = int(((deg[rows] - 1) * (deg[nb] - 1)).sum()) - tr3
+    assert deg.max() >= 512                      # hub lists: many 128-element rounds
+    g = gm.gm_load_graph(n, s, d)
+    q = gi.Query(4, [(0, 1), (1, 2), (2, 3)], [0, 0, 0, 0])
+    for budget, mindeg in ((64 << 20, 64), (0, 64)):       # hub bitmaps / binary search only
+        g.build_hubs(budget, mindeg)
+        p = gm.gm_plan_query(g, q, order=[1, 2, 0, 3])
+        for tau in (1, 10 ** 6):
+            c, st = gm.gm_count(p, tau=tau, symmetry=False)
+            assert st["paths"] & 2, st             # pair counting ran
+            assert c == want, (budget, tau, c, want)
+        assert gm.gm_count(p, pair_count=False, symmetry=False)[0] == want
+        assert gm.gm_count(p)[0] == want
+
+
+def test_enumerate_stop_at_capacity(gm):
+    """GM_FLAG_STOP_AT_CAPACITY: the search stops once the buffer is full; every written row is
+    a distinct embedding (a subset of the oracle's set) and the reported count is >= capacity."""
+    n, s, d = gi.rmat_edges(10, 8, 31)
+    lab = gi.uniform_labels(n, 2, 31)
+    q = small_random_query(31, 5, 2)
+    og = OracleGraph(n, s, d, lab)
+    ref = og.enumerate(q)
+    assert len(ref) > 5000
+    g = gm.gm_load_graph(n, s, d, lab, 2)
+    p = gm.gm_plan_query(g, q)
+    refset = {tuple(r) for r in ref.tolist()}
+    for tau in (1, 10 ** 6):
+        rows, total, st = gm.gm_enumerate(p, capacity=1000, tau=tau, stop_at_capacity=True)
+        assert total >= 1000 and len(rows) == 1000
+        got = {tuple(r) for r in rows.tolist()}
+        assert len(got) == 1000 and got <= refset
+    rows, total, st = gm.gm_enumerate(p, capacity=len(ref) + 10, stop_at_capacity=True)
+    assert total == len(ref) and st["timed_out"] == 0

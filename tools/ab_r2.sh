@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round-2 same-box A/B: build variants, then time each on rmat24 (all roots, 1 s limit: tasks
+# done), rmat18 pair-counting queries (300 ms limit) and rmat18 dense queries (100 roots).
+#   tools/ab_r2.sh OUTDIR  "name:flags" ...      ("cur:" = the in-tree build)
+OUT=$1; shift
+mkdir -p $OUT
+LIBS=()
+for spec in "$@"; do
+  name=${spec%%:*}; flags=${spec#*:}
+  if [ "$name" = cur ]; then LIBS+=(""); continue; fi
+  tools/build_variant.sh /tmp/gm_$name.so paper_2604_10601_b200/csrc $flags && LIBS+=(/tmp/gm_$name.so)
+done
+run() {  # cfg nroots limit qi...
+  local cfg=$1 nr=$2 lim=$3; shift 3
+  for qi in "$@"; do
+    for lib in "${LIBS[@]}"; do
+      GM_LIB=$lib GM_LIMIT_MS=$lim timeout 300 python tools/profile_one.py $qi $nr $cfg 2>&1 | tail -1 | cut -c1-200 | sed "s|^|[${lib:-cur}] $cfg q$qi |"
+    done
+  done
+}
+run rmat18 0 300 4 5 6 7 > $OUT/ab_rmat18_pair.log 2>&1
+run rmat18 100 0 0 1 2 3 > $OUT/ab_rmat18_dense.log 2>&1
+run rmat24 0 1000 0 1 2 3 > $OUT/ab_rmat24.log 2>&1
