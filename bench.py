@@ -35,6 +35,12 @@ CONFIGS = {
     # name: (generator, params, labels, query size, dense seeds, sparse seeds, time limit ms)
     "rmat18": dict(kind="rmat", scale=18, ef=16, labels=8, qsize=8, dense=[1000, 1001, 1002, 1003],
                    sparse=[2000, 2001, 2002, 2003], limit_ms=1000.0, seed=2,
+                   # the dense queries that complete (profiles/r02/explore_bench18.log: rq8_s1000
+                   # and the four random-walk trees are still unsolved after 30 s), run without a
+                   # binding limit once per bench as the latency leg
+                   complete=dict(sizes=[8, 8, 8], seeds=[1001, 1002, 1003]), complete_limit_ms=60000.0,
+                   complete_desc="rq8_s1001..1003 (dense 8-vertex, solved in 0.5-5 s); rq8_s1000 and "
+                                 "wq8_s2000..2003 exceed 30 s",
                    desc="R-MAT scale 18 (262k vertices, ~3.8M edges, 8 labels), 8-vertex dense+sparse queries"),
     "er1k": dict(kind="er", n=1000, deg=8, labels=4, qsize=4, dense=[], sparse=[], fixed="tailed_triangle",
                  limit_ms=0.0, seed=11, desc="Erdos-Renyi G(n=1000, avg deg 8, 4 labels), tailed triangle"),
@@ -284,6 +290,8 @@ def main():
                          "query explores a uniform sample of its roots) or device-id order (hubs first)")
     ap.add_argument("--static-roots", action="store_true",
                     help="N > 1: static (v/64) %% N root partition instead of the shared pool counter")
+    ap.add_argument("--no-team", action="store_true",
+                    help="N > 1: no cross-GPU stealing (idle warps steal only within their GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-context", action="store_true", help="skip the context legs (hubs-first order, "
                     "Alg. 2 as written, gm_enumerate, the complete query set)")
@@ -351,6 +359,12 @@ def main():
         if rank != 0:
             shared_ptr = gm.gm_pool_counter_open(box[0])
         run_kw = dict(tau=int(args.tau), steal=not args.no_steal, time_limit_ms=limit, root_seed=root_seed)
+        if not args.no_team and not args.no_steal:
+            # cross-GPU stealing: every rank maps every other rank's steal ring and work word
+            handles = [None] * world
+            dist.all_gather_object(handles, gm.gm_team_export())
+            team = gm.gm_team_open(world, rank, handles)
+            run_kw["team"] = team
 
     counts_dev = torch.zeros(nslots, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -607,6 +621,7 @@ def main():
                    "parallelism": ("1 GPU, whole pool on one device" if world == 1 else
                                    f"{world} GPU(s), CSR replicated, " +
                                    ("pool batches claimed from shared counters (NVLink peer system-scope atomics)"
+                                    + (", cross-GPU stealing (gm_team)" if "team" in run_kw else "")
                                     if shared_ptr is not None else "static root partition") +
                                    ", 1 all-reduce of the counts per step")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -62,6 +62,7 @@ extern "C" {
 
 typedef struct gm_graph gm_graph;
 typedef struct gm_plan gm_plan;
+typedef struct gm_team gm_team;
 
 /* ------------------------------------------------------------------ graph */
 
@@ -170,6 +171,9 @@ GM_API void gm_free_plan(gm_plan *p);
 #define GM_FLAG_STOP_AT_CAPACITY 8u /* gm_enumerate: stop the search once `capacity` rows are
                                     written (returns GM_TIMEOUT; *count_host is then the number
                                     found so far, >= capacity) -- for timing row output */
+#define GM_FLAG_NO_POOL      16u /* diagnostic (tests): this rank claims no pool batches and gets
+                                    work only by stealing (needs steal = 1; with a team, from
+                                    other ranks' rings) */
 #define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
                                     Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)|.
                                     Symmetry breaking is also skipped when `roots` is given. */
@@ -200,6 +204,14 @@ typedef struct {
                                 explores a uniform sample of the roots (the BFS pool keeps the
                                 root order).  Counts of completed runs never depend on it; ranks
                                 sharing a pool counter must pass the same seed. */
+    gm_team *team;           /* optional stealing team (gm_team_open): idle warps also pop the
+                                steal rings of the other ranks and post requests to them, and
+                                the DFS ends when the whole team is out of work (cross-GPU
+                                stealing, §4.3 "replicated at the block level
+                                using global memory", one level up).  Every rank of the team
+                                runs the same query with the same shared_pool_ctr slot (needed)
+                                and the same options (time limits included); see gm_team_open
+                                for the protocol.  NULL: stealing stays within this GPU. */
 } gm_run_opts;
 
 GM_API void gm_default_opts(gm_run_opts *o);
@@ -283,6 +295,38 @@ GM_API int gm_pool_counter_create(uint32_t slots, void **counter_dev, void *ipc_
 GM_API int gm_pool_counter_open(const void *ipc_handle, void **counter_dev);
 GM_API int gm_pool_counter_reset(void *counter_dev, uint32_t slots, void *stream);
 GM_API int gm_pool_counter_close(void *counter_dev, int owner);
+
+/* ------------------------------------------------------------------ cross-GPU stealing team */
+
+/*
+ * A team of ranks (processes, one per GPU of a node) whose DFS kernels steal from each other
+ * over NVLink peer memory, the paper's dynamic balancing phase (§4.3:
+ * idle warps receive half of a busy warp's execution stack; "the same mechanism is replicated
+ * at the block level using global memory") taken one level further, to GPUs.
+ *   gm_team_export: allocate this device's search workspace (control block + steal ring) if
+ *       needed and copy GM_TEAM_HANDLE_BYTES of CUDA IPC handles for it into handle_out.
+ *   gm_team_open: world (1..8) ranks' exported handles, concatenated in rank order
+ *       (world * GM_TEAM_HANDLE_BYTES bytes); maps every other rank's workspace into this
+ *       process and returns a team handle for gm_run_opts.team.  Call on the device the
+ *       searches will run on, after every rank exported.
+ *   gm_team_free: unmap (call after the last search that uses the team).
+ * Protocol: the ranks run the same sequence of searches with the team; search k runs on every
+ * rank with the same plan inputs, options and shared_pool_ctr slot (a shared pool counter is
+ * required: every rank then builds the same pool).  No barrier is needed between searches:
+ * the team numbers its searches (epoch k, the same on every rank), every steal item carries
+ * its epoch and is popped only by warps of that epoch, and each rank's work word is
+ * (epoch << 32) | count.  Termination: a unit of work is counted in the lineage rank that
+ * claimed its pool batch, wherever it runs; once the pool is exhausted a lineage count only
+ * decreases, and a word tagged with another epoch holds none of this search's units, so a
+ * rank ends its DFS when every rank's word reads zero for its epoch.  Memory model: the
+ * team's counters, ring positions and slot sequence numbers use system-scope atomics and
+ * acquire loads; items are written before a __threadfence_system() and the slot's sequence
+ * store that publishes them.
+ */
+#define GM_TEAM_HANDLE_BYTES 256
+GM_API int gm_team_export(void *handle_out);
+GM_API int gm_team_open(uint32_t world, uint32_t rank, const void *handles, gm_team **out);
+GM_API void gm_team_free(gm_team *t);
 
 /* Thread-local description of the last error (empty string if none). */
 GM_API const char *gm_last_error(void);

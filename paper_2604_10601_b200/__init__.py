@@ -178,7 +178,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
           time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True, pair_count=True,
-          shared_pool_ctr=None, root_seed=0, stop_at_capacity=False):
+          shared_pool_ctr=None, root_seed=0, stop_at_capacity=False, team=None, no_pool=False):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -208,6 +208,10 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.flags |= L.GM_FLAG_NO_SYMMETRY
     if stop_at_capacity:
         o.flags |= L.GM_FLAG_STOP_AT_CAPACITY
+    if no_pool:
+        o.flags |= L.GM_FLAG_NO_POOL
+    if team is not None:
+        o.team = team._h
     if shared_pool_ctr is not None:
         o.shared_pool_ctr = ctypes.c_void_p(int(shared_pool_ctr))
     o.root_seed = int(root_seed)
@@ -237,6 +241,43 @@ def pool_counter_slot(ptr, k: int):
 
 def gm_pool_counter_reset(ptr, slots: int = 1, stream=None):
     L.check(L.lib().gm_pool_counter_reset(ctypes.c_void_p(ptr), int(slots), _stream_handle(stream)))
+
+
+class Team:
+    """Handle of a cross-GPU stealing team (gm_team_open); pass as gm_count(..., team=t)."""
+
+    def __init__(self, handle, world, rank):
+        self._h = ctypes.c_void_p(handle)
+        self.world, self.rank = world, rank
+
+    def free(self):
+        if self._h and self._h.value:
+            L.lib().gm_team_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def gm_team_export() -> bytes:
+    """IPC handles of this device's search workspace (control block + steal ring)."""
+    h = (ctypes.c_char * L.GM_TEAM_HANDLE_BYTES)()
+    L.check(L.lib().gm_team_export(h))
+    return bytes(h)
+
+
+def gm_team_open(world: int, rank: int, handles) -> Team:
+    """Map every rank's exported workspace; handles = list of gm_team_export() bytes, rank order."""
+    blob = b"".join(bytes(x) for x in handles)
+    if len(blob) != world * L.GM_TEAM_HANDLE_BYTES:
+        raise ValueError("need one exported handle per rank")
+    buf = (ctypes.c_char * len(blob)).from_buffer_copy(blob)
+    h = ctypes.c_void_p(0)
+    L.check(L.lib().gm_team_open(int(world), int(rank), buf, ctypes.byref(h)))
+    return Team(h.value, world, rank)
 
 
 def gm_pool_counter_close(ptr, owner: bool):

@@ -22,6 +22,8 @@ GM_FLAG_NO_SET_COUNT = 1
 GM_FLAG_NO_SYMMETRY = 2
 GM_FLAG_NO_PAIR_COUNT = 4
 GM_FLAG_STOP_AT_CAPACITY = 8
+GM_FLAG_NO_POOL = 16
+GM_TEAM_HANDLE_BYTES = 256
 GM_PATH_SET_COUNT, GM_PATH_PAIR_COUNT, GM_PATH_PAR_CHECKS, GM_PATH_SYMMETRY = 1, 2, 4, 8
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 
@@ -31,6 +33,7 @@ EXPORTS = [
     "gm_plan_query", "gm_plan_info", "gm_plan_candidates", "gm_free_plan",
     "gm_default_opts", "gm_count", "gm_enumerate", "gm_last_error", "gm_version",
     "gm_pool_counter_create", "gm_pool_counter_open", "gm_pool_counter_reset", "gm_pool_counter_close",
+    "gm_team_export", "gm_team_open", "gm_team_free",
 ]
 GM_IPC_HANDLE_BYTES = 64
 GM_POOL_COUNTER_STRIDE = 128
@@ -54,7 +57,8 @@ class RunOpts(ctypes.Structure):
                 ("blocks_per_sm", ctypes.c_uint32), ("warps_per_block", ctypes.c_uint32),
                 ("time_limit_ms", ctypes.c_double), ("roots", ctypes.POINTER(ctypes.c_uint32)),
                 ("num_roots", ctypes.c_uint64), ("pool_bytes_max", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("shared_pool_ctr", ctypes.c_void_p), ("root_seed", ctypes.c_uint64)]
+                ("flags", ctypes.c_uint32), ("shared_pool_ctr", ctypes.c_void_p), ("root_seed", ctypes.c_uint64),
+                ("team", ctypes.c_void_p)]
 
 
 class RunStats(ctypes.Structure):
@@ -104,6 +108,10 @@ def lib():
         L.gm_pool_counter_open.argtypes = [vp, ctypes.POINTER(vp)]
         L.gm_pool_counter_reset.argtypes = [vp, ctypes.c_uint32, vp]
         L.gm_pool_counter_close.argtypes = [vp, ctypes.c_int]
+        L.gm_team_export.argtypes = [vp]
+        L.gm_team_open.argtypes = [ctypes.c_uint32, ctypes.c_uint32, vp, ctypes.POINTER(vp)]
+        L.gm_team_free.argtypes = [vp]
+        L.gm_team_free.restype = None
         L.gm_last_error.restype = ctypes.c_char_p
         L.gm_version.restype = ctypes.c_char_p
         _lib = L

@@ -58,20 +58,21 @@ constexpr uint32_t FULL = 0xffffffffu;
 // 16/32-level kernels: the WarpStack (7.8 / 15.6 KB per warp) limits residency to ~6 / ~3 blocks
 // per SM, so they may use the registers that frees
 #ifndef GM_MINB16
-#define GM_MINB16 6
+#define GM_MINB16 9
 #endif
 #ifndef GM_MINB32
-#define GM_MINB32 3
+#define GM_MINB32 9
 #endif
 #define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? GM_MINB16 : GM_MINB32))
 #ifndef GM_TWO_VEC
 #define GM_TWO_VEC 1       // pair-counting intersection: 128-element rounds with 16-byte loads
 #endif
 #ifndef GM_PROBES_WIDE
-#define GM_PROBES_WIDE 4   // probes in flight per lane in the 16/32-level kernels (process())
-#endif
+#define GM_PROBES_WIDE 2   // probes in flight per lane in the 16/32-level kernels (process()); 4 was
+#endif                     // measured 13-51 % fewer tasks/s on rmat24 (wasted probes)
 constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
-constexpr uint32_t kItemWords = 4 + kMaxQ;     // [depth, cb, cl, cs, prefix[kMaxQ]]
+constexpr uint32_t kItemWords = 6 + kMaxQ;     // [depth, cb, cl, cs, home, epoch, prefix[kMaxQ]]
+constexpr uint32_t kMaxTeam = 8;               // ranks of a stealing team (gm_team)
 
 // Global control block.  Every field that many warps poll or update lives on its own
 // 128-byte line so that the pollers of one do not serialise the atomics of another.
@@ -82,6 +83,7 @@ struct Ctrl {
     alignas(128) unsigned long long q_head;   // ring positions (monotone, 64-bit: never wrap)
     alignas(128) unsigned long long q_tail;
     alignas(128) int abort;
+    alignas(128) unsigned long long tword;    // team: (epoch << 32) | lineage work count
     unsigned long long t0;                    // globaltimer at the first warp's start
     alignas(128) unsigned long long out_ctr;
     alignas(128) unsigned long long count;
@@ -148,6 +150,16 @@ struct SearchParams {
     uint32_t *out;              // enumerate rows (nq words each)
     unsigned long long out_cap;
     uint32_t stop_at_cap;       // enumerate: stop once out_cap rows are written
+    // cross-GPU stealing (gm_team): every rank's control block and steal ring mapped through
+    // peer memory; team_n = 0 when this launch steals only within its GPU.  A unit of work is
+    // counted in the `work` word of its lineage rank (`home`: the rank whose pool batch it
+    // came from), wherever it runs, so a rank's count, once zero with the pool exhausted,
+    // stays zero and the team terminates when every rank's count reads zero.
+    uint32_t team_n, team_rank, epoch;      // epoch: this search's number in the team's sequence
+    Ctrl *team_ctrl[kMaxTeam];
+    uint32_t *team_items[kMaxTeam];
+    unsigned long long *team_seq[kMaxTeam];
+    uint32_t no_pool;           // GM_FLAG_NO_POOL (diagnostic): take no pool batches, only steal
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
 };
 
@@ -228,6 +240,60 @@ __device__ __forceinline__ unsigned long long pool_peek(const SearchParams &P) {
 }
 __device__ __forceinline__ unsigned long long pool_claim(const SearchParams &P, unsigned long long n) {
     return P.pool_sys ? atomicAdd_system(P.pool_ctr, n) : atomicAdd(P.pool_ctr, n);
+}
+
+// Scope-dependent atomics of the steal protocol: a team's counters and rings are touched by
+// several GPUs, so they take system-scope atomics and loads; alone, device scope.
+__device__ __forceinline__ int ld_sys(const int *p) {
+    int x;
+    asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    return x;
+}
+__device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long *p) {
+    unsigned long long x;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+    return x;
+}
+__device__ __forceinline__ unsigned long long ld_sys64(const unsigned long long *p) {
+    unsigned long long x;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+    return x;
+}
+// Team counts live in the low half of (epoch << 32) | count: a rank's word tagged with another
+// epoch holds no unit of this search (the rank has not started it, or has finished it, which
+// needs its lineage count at zero), so consecutive searches need no barrier between them.
+__device__ __forceinline__ void work_add(const SearchParams &P, Ctrl *C, uint32_t home, int delta) {
+    if (P.team_n) atomicAdd_system(&P.team_ctrl[home]->tword, (unsigned long long)(long long)delta);
+    else atomicAdd(&C->work, delta);
+}
+__device__ __forceinline__ int req_add(const SearchParams &P, Ctrl *C, int delta) {
+    return P.team_n ? atomicAdd_system(&C->requests, delta) : atomicAdd(&C->requests, delta);
+}
+// every rank's lineage count is zero (the whole team is out of work)
+__device__ __forceinline__ bool team_idle(const SearchParams &P, volatile Ctrl *VC) {
+    if (!P.team_n) return VC->work == 0;
+    for (uint32_t r = 0; r < P.team_n; ++r) {
+        const unsigned long long w = ld_sys64(&P.team_ctrl[r]->tword);
+        if ((uint32_t)(w >> 32) == P.epoch && (uint32_t)w != 0) return false;
+    }
+    return true;
+}
+// Pop one item from rank r's ring (r = this rank: its own ring); returns its position or ~0.
+__device__ __forceinline__ unsigned long long ring_pop(const SearchParams &P, Ctrl *C, uint32_t r) {
+    if (!P.team_n) {
+        volatile Ctrl *VC = C;
+        const unsigned long long pos = VC->q_head;
+        const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
+        return (seq == pos + 1 && atomicCAS(&C->q_head, pos, pos + 1) == pos) ? pos : ~0ull;
+    }
+    Ctrl *RC = P.team_ctrl[r];
+    const unsigned long long pos = ld_acq_sys(&RC->q_head);
+    const unsigned long long seq = ld_acq_sys(P.team_seq[r] + pos % P.q_cap);
+    if (seq != pos + 1) return ~0ull;
+    // an item published for another search of the team (that rank is ahead or behind): skip
+    const uint32_t ep = ((const volatile uint32_t *)P.team_items[r])[(pos % P.q_cap) * kItemWords + 5];
+    if (ep != P.epoch) return ~0ull;
+    return atomicCAS_system(&RC->q_head, pos, pos + 1) == pos ? pos : ~0ull;
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -346,9 +412,9 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
     // G checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
     // independent, so each lane keeps G dependent-load chains in flight (ncu: the kernel is
-    // bound by long-scoreboard stalls on its probes, not by bandwidth).  G = 2 for the
-    // L2-resident small-query kernel (issue-bound: fewer wasted probes), 4 for the 16/32-level
-    // kernels that run the DRAM-resident configs (more memory-level parallelism per warp).
+    // bound by long-scoreboard stalls on its probes, not by bandwidth).  A larger G wastes the
+    // probes of tasks that fail an earlier check of the group (most do): G = 4 in the 16/32-level
+    // kernels cost 13-51 % of rmat24's tasks/s, so G = 2 everywhere by default.
     constexpr int G = D <= 8 ? 2 : GM_PROBES_WIDE;
     for (int c = 0; c < nchk; c += G) {
         if (!__any_sync(FULL, ok)) break;
@@ -795,6 +861,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
     uint32_t tick = 0;
     bool stop = false;
     bool registered = false;   // this idle warp has posted a steal request
+    uint32_t home = P.team_rank;   // lineage rank of the unit this warp holds (gm_team)
+    uint32_t idle_polls = 0;       // failed polls since this warp went idle (team: remote requests)
     // time limit relative to this launch: the first warp to start stamps t0
     if (P.limit_ns && lane == 0) atomicCAS(&C->t0, 0ull, globaltimer());
 
@@ -803,30 +871,39 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
         int base = 0, l = 0;
         bool got = false;
         uint32_t backoff = 64;
+        uint32_t src_rank = P.team_rank;     // ring the popped item came from
         while (true) {
             unsigned long long b = ~0ull, item = ~0ull;
             int exit_now = 0;
             if (lane == 0) {
                 if (VC->abort) {
                     exit_now = 1;
-                } else if (pool_peek(P) < P.pool_size) {
-                    atomicAdd(&C->work, 1);
+                } else if (!P.no_pool && pool_peek(P) < P.pool_size) {
+                    work_add(P, C, P.team_rank, 1);
                     // P.pool_ctr: this launch's counter, or one shared by every rank's launch
                     // (peer memory over NVLink: multi-GPU dynamic chunk assignment)
                     b = pool_claim(P, (unsigned long long)P.batch);
-                    if (b >= P.pool_size) { atomicSub(&C->work, 1); b = ~0ull; }
+                    if (b >= P.pool_size) { work_add(P, C, P.team_rank, -1); b = ~0ull; }
                 }
                 if (!exit_now && b == ~0ull) {
                     if (!P.steal) {
                         exit_now = 1;
                     } else {
-                        if (!registered) { atomicAdd(&C->requests, 1); registered = true; }
-                        // pop (bounded MPMC ring, per-slot sequence numbers)
-                        const unsigned long long pos = VC->q_head;
-                        const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
-                        if (seq == pos + 1 && atomicCAS(&C->q_head, pos, pos + 1) == pos) item = pos;
-                        if (item == ~0ull && pool_peek(P) >= P.pool_size &&
-                            VC->work == 0)
+                        if (!registered) { req_add(P, C, 1); registered = true; idle_polls = 0; }
+                        // pop (bounded MPMC ring, per-slot sequence numbers): own ring first,
+                        // then (team) the other ranks' rings over peer memory
+                        item = ring_pop(P, C, P.team_rank);
+                        src_rank = P.team_rank;
+                        for (uint32_t k = 1; k < P.team_n && item == ~0ull; ++k) {
+                            src_rank = (P.team_rank + k) % P.team_n;
+                            item = ring_pop(P, C, src_rank);
+                        }
+                        if (item == ~0ull && P.team_n > 1 && (++idle_polls & 31u) == 0) {
+                            // still idle: ask the next rank's busy warps to split their stacks
+                            const uint32_t r = (P.team_rank + 1 + (idle_polls >> 5) % (P.team_n - 1)) % P.team_n;
+                            atomicAdd_system(&P.team_ctrl[r]->requests, 1);
+                        }
+                        if (item == ~0ull && pool_peek(P) >= P.pool_size && team_idle(P, VC))
                             exit_now = 1;
                     }
                 }
@@ -834,9 +911,11 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             }
             b = __shfl_sync(FULL, b, 0);
             item = __shfl_sync(FULL, item, 0);
+            src_rank = __shfl_sync(FULL, src_rank, 0);
             exit_now = __shfl_sync(FULL, exit_now, 0);
             if (exit_now) { stop = true; break; }
             if (b != ~0ull) {
+                home = P.team_rank;             // a pool batch: this rank's lineage
                 // pool batch: up to `batch` partial matches of depth d0 become the lanes of level d0-1
                 const unsigned long long k = min((unsigned long long)P.batch, P.pool_size - b);
                 const bool valid = lane < k;
@@ -855,18 +934,30 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 break;
             }
             if (item != ~0ull) {
-                __threadfence();
+                // lane 0's acquire load of the slot's sequence number, then this warp barrier
+                // (memory-ordering among the lanes), then every lane's strong item loads
+                if (P.team_n) __threadfence_system(); else __threadfence();
+                __syncwarp();
                 const unsigned long long slot = item % P.q_cap;
-                const uint32_t *it = P.q_items + slot * kItemWords;
-                const uint32_t depth = __ldcg(it);     // written by another SM: read through L2
-                if (lane < depth) { S.v[lane][0] = __ldcg(it + 4 + lane); S.pid[lane][0] = 0; }
-                S.cb[depth][lane] = lane == 0 ? __ldcg(it + 1) : 0;
-                S.cl[depth][lane] = lane == 0 ? __ldcg(it + 2) : 0;
-                S.cs[depth][lane] = (uint8_t)(lane == 0 ? __ldcg(it + 3) : 0);
+                // written by another SM (or, in a team, another GPU): volatile loads, which
+                // are strong at system scope (LDG.E.STRONG.SYS), never a stale L1 line
+                const volatile uint32_t *it =
+                    (P.team_n ? P.team_items[src_rank] : P.q_items) + slot * kItemWords;
+                const uint32_t depth = it[0];
+                if (lane < depth) { S.v[lane][0] = it[6 + lane]; S.pid[lane][0] = 0; }
+                S.cb[depth][lane] = lane == 0 ? it[1] : 0;
+                S.cl[depth][lane] = lane == 0 ? it[2] : 0;
+                S.cs[depth][lane] = (uint8_t)(lane == 0 ? it[3] : 0);
+                home = __shfl_sync(FULL, lane == 0 ? it[4] : 0u, 0);
                 __syncwarp();
                 if (lane == 0) {   // release the slot for the next lap of the ring
-                    __threadfence();
-                    ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
+                    if (P.team_n) {
+                        __threadfence_system();
+                        ((volatile unsigned long long *)P.team_seq[src_rank])[slot] = item + P.q_cap;
+                    } else {
+                        __threadfence();
+                        ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
+                    }
                 }
                 if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, scr, depth, lane == 0, lane);
                 if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
@@ -890,9 +981,9 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     if (P.limit_ns && globaltimer() > VC->t0 + P.limit_ns) atomicExch(&C->abort, 1);
                     ab = VC->abort;
                     // work stealing (§4.3): serve one posted request by splitting our stack
-                    if (P.steal && VC->requests > 0) {
-                        if (atomicSub(&C->requests, 1) > 0) claim = 1;
-                        else atomicAdd(&C->requests, 1);
+                    if (P.steal && (P.team_n ? ld_sys(&C->requests) : VC->requests) > 0) {
+                        if (req_add(P, C, -1) > 0) claim = 1;
+                        else req_add(P, C, 1);
                     }
                 }
                 if (__shfl_sync(FULL, ab, 0)) { stop = true; break; }
@@ -922,10 +1013,12 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         // reserve a ring slot
                         unsigned long long pos = ~0ull;
                         if (lane == 0) {
-                            atomicAdd(&C->work, 1);
+                            work_add(P, C, home, 1);          // the new unit keeps this unit's lineage
                             pos = VC->q_tail;
                             while (true) {
-                                const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
+                                // (slots are released by poppers, possibly on other GPUs)
+                                const unsigned long long seq = P.team_n ? ld_acq_sys(P.q_seq + pos % P.q_cap)
+                                                                        : ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
                                 if (seq == pos) {
                                     const unsigned long long prev = atomicCAS(&C->q_tail, pos, pos + 1);
                                     if (prev == pos) break;
@@ -937,22 +1030,23 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                                     pos = VC->q_tail;
                                 }
                             }
-                            if (pos == ~0ull) atomicSub(&C->work, 1);
+                            if (pos == ~0ull) work_add(P, C, home, -1);
                         }
                         pos = __shfl_sync(FULL, pos, 0);
                         if (pos == ~0ull) break;          // ring full: keep the work
                         if (lane == giver) {
                             uint32_t *it = P.q_items + (pos % P.q_cap) * kItemWords;
                             it[0] = (uint32_t)s; it[1] = S.cb[s][giver] + gb; it[2] = give; it[3] = S.cs[s][giver];
-                            read_prefix<D>(S, s - 1, giver, it + 4);
+                            it[4] = home; it[5] = P.epoch;
+                            read_prefix<D>(S, s - 1, giver, it + 6);
                             S.cl[s][giver] = mask ? 0u : gb;
-                            __threadfence();
+                            if (P.team_n) __threadfence_system(); else __threadfence();
                             ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap] = pos + 1;
                         }
                         served = 1;
                         my_don += (lane == 0);
                     }
-                    if (!served && lane == 0) atomicAdd(&C->requests, 1);   // give the request back
+                    if (!served && lane == 0) req_add(P, C, 1);   // give the request back
                     __syncwarp();
                 }
             }
@@ -1067,7 +1161,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             __syncwarp();
             ++l;
         }
-        if (lane == 0) atomicSub(&C->work, 1);
+        if (lane == 0) work_add(P, C, home, -1);
     }
     // flush counters
     my_words += wacc;
@@ -1336,6 +1430,26 @@ static Workspace *device_workspace(int dev) {
     return d.ws;
 }
 
+static int workspace_alloc_ring(Workspace &W) {
+    if (!W.ctrl) GM_CK(cudaMalloc(&W.ctrl, sizeof(Ctrl)));
+    if (!W.q_items) {
+        W.q_cap = 1u << 18;
+        GM_CK(cudaMalloc(&W.q_items, sizeof(uint32_t) * (size_t)W.q_cap * kItemWords));
+        GM_CK(cudaMalloc(&W.q_seq, sizeof(unsigned long long) * (size_t)W.q_cap));
+    }
+    return GM_OK;
+}
+
+// A stealing team: every rank's control block and steal ring, mapped into this process.
+struct gm_team {
+    uint32_t n = 0, rank = 0;
+    int dev = 0;
+    uint32_t epoch = 0;      // searches run with this team so far (the same sequence on every rank)
+    Ctrl *ctrl[kMaxTeam] = {};
+    uint32_t *items[kMaxTeam] = {};
+    unsigned long long *seq[kMaxTeam] = {};
+};
+
 extern "C" void gm_default_opts(gm_run_opts *o) {
     if (!o) return;
     memset(o, 0, sizeof(*o));
@@ -1375,6 +1489,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     GM_REQ(o.warps_per_block <= kDfsMaxWarps, GM_ERR_ARG, "warps_per_block %u > %u (k_dfs launch bounds)",
            o.warps_per_block, kDfsMaxWarps);
     GM_REQ(o.num_roots == 0 || o.roots, GM_ERR_ARG, "num_roots > 0 but roots NULL");
+    GM_REQ(!o.team || (o.steal && o.shared_pool_ctr), GM_ERR_ARG,
+           "a stealing team needs steal = 1 and a shared pool counter (every rank builds the same pool)");
+    GM_REQ(!(o.flags & GM_FLAG_NO_POOL) || o.steal, GM_ERR_ARG, "GM_FLAG_NO_POOL needs steal = 1");
     const gm_graph *g = p->g;
     int dev = 0;
     GM_CK(cudaGetDevice(&dev));
@@ -1581,10 +1698,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
 
     // ---- DFS (fine-grained, batch exploration, stealing)
     if (!done) {
-        if (o.steal && !W.q_items) {
-            W.q_cap = 1u << 18;
-            GM_CK(cudaMalloc(&W.q_items, sizeof(uint32_t) * (size_t)W.q_cap * kItemWords));
-            GM_CK(cudaMalloc(&W.q_seq, sizeof(unsigned long long) * (size_t)W.q_cap));
+        if (o.steal) {
+            rc = workspace_alloc_ring(W);
+            if (rc) return rc;
         }
         if (o.steal) {
             k_init_ring<<<grid_for(W.q_cap, 256, W.sms), 256, 0, st>>>(W.q_seq, W.q_cap);
@@ -1600,6 +1716,24 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         P.d0 = d;
         P.steal = o.steal ? 1 : 0;
         P.q_items = W.q_items; P.q_seq = W.q_seq; P.q_cap = o.steal ? W.q_cap : 1;
+        P.no_pool = (o.flags & GM_FLAG_NO_POOL) ? 1u : 0u;
+        if (o.team) {
+            gm_team *t = o.team;
+            GM_REQ(t->dev == dev && t->ctrl[t->rank] == W.ctrl && t->items[t->rank] == W.q_items,
+                   GM_ERR_ARG, "gm_run_opts.team was opened on another device or process state");
+            P.team_n = t->n;
+            P.team_rank = t->rank;
+            P.epoch = ++t->epoch;
+            // this rank's lineage word for the new search: (epoch << 32) | 0, published before
+            // the DFS launch (the control block was just zeroed)
+            const unsigned long long tw = (unsigned long long)P.epoch << 32;
+            GM_CK(cudaMemcpyAsync(&W.ctrl->tword, &tw, sizeof(tw), cudaMemcpyHostToDevice, st));
+            for (uint32_t r = 0; r < t->n; ++r) {
+                P.team_ctrl[r] = t->ctrl[r];
+                P.team_items[r] = t->items[r];
+                P.team_seq[r] = t->seq[r];
+            }
+        }
         if (enumerate) {
             P.out = out_dev(); P.out_cap = cap;
             P.stop_at_cap = (o.flags & GM_FLAG_STOP_AT_CAPACITY) ? 1u : 0u;
@@ -1762,6 +1896,79 @@ extern "C" int gm_enumerate(const gm_plan *p, const gm_run_opts *opts, uint32_t 
                             uint64_t *count_host, gm_run_stats *stats, void *stream) {
     GM_REQ(capacity == 0 || out, GM_ERR_ARG, "gm_enumerate: out NULL with capacity > 0");
     return run_search(p, opts, true, out, capacity, mem, count_host, GM_MEM_HOST, stats, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ cross-GPU stealing team
+
+extern "C" int gm_team_export(void *handle_out) {
+    set_error("");
+    GM_REQ(handle_out, GM_ERR_ARG, "gm_team_export: NULL handle_out");
+    static_assert(3 * sizeof(cudaIpcMemHandle_t) <= GM_TEAM_HANDLE_BYTES, "team handle size");
+    int dev = 0;
+    GM_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_ws[dev & 63].mu);
+    Workspace &W = *device_workspace(dev);
+    int rc = workspace_alloc_ring(W);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h[3];
+    GM_CK(cudaIpcGetMemHandle(&h[0], W.ctrl));
+    GM_CK(cudaIpcGetMemHandle(&h[1], W.q_items));
+    GM_CK(cudaIpcGetMemHandle(&h[2], W.q_seq));
+    memset(handle_out, 0, GM_TEAM_HANDLE_BYTES);
+    memcpy(handle_out, h, sizeof(h));
+    return GM_OK;
+}
+
+extern "C" int gm_team_open(uint32_t world, uint32_t rank, const void *handles, gm_team **out) {
+    set_error("");
+    GM_REQ(handles && out, GM_ERR_ARG, "gm_team_open: NULL argument");
+    GM_REQ(world >= 1 && world <= kMaxTeam && rank < world, GM_ERR_ARG, "gm_team_open: world %u rank %u (max %u)",
+           world, rank, kMaxTeam);
+    int dev = 0;
+    GM_CK(cudaGetDevice(&dev));
+    Workspace *W = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_ws[dev & 63].mu);
+        W = device_workspace(dev);
+        int rc = workspace_alloc_ring(*W);
+        if (rc) return rc;
+    }
+    gm_team *t = new gm_team();
+    t->n = world; t->rank = rank; t->dev = dev;
+    const uint8_t *hb = static_cast<const uint8_t *>(handles);
+    for (uint32_t r = 0; r < world; ++r) {
+        if (r == rank) {
+            t->ctrl[r] = W->ctrl; t->items[r] = W->q_items; t->seq[r] = W->q_seq;
+            continue;
+        }
+        cudaIpcMemHandle_t h[3];
+        memcpy(h, hb + (size_t)r * GM_TEAM_HANDLE_BYTES, sizeof(h));
+        void *p[3] = {nullptr, nullptr, nullptr};
+        cudaError_t e = cudaSuccess;
+        for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaIpcOpenMemHandle(&p[k], h[k], cudaIpcMemLazyEnablePeerAccess);
+        t->ctrl[r] = static_cast<Ctrl *>(p[0]);
+        t->items[r] = static_cast<uint32_t *>(p[1]);
+        t->seq[r] = static_cast<unsigned long long *>(p[2]);
+        if (e != cudaSuccess) {
+            gm_team_free(t);
+            cudaGetLastError();
+            set_error("gm_team_open: cudaIpcOpenMemHandle for rank %u: %s", r, cudaGetErrorString(e));
+            return GM_ERR_CUDA;
+        }
+    }
+    *out = t;
+    return GM_OK;
+}
+
+extern "C" void gm_team_free(gm_team *t) {
+    if (!t) return;
+    for (uint32_t r = 0; r < t->n; ++r) {
+        if (r == t->rank) continue;
+        if (t->ctrl[r]) cudaIpcCloseMemHandle(t->ctrl[r]);
+        if (t->items[r]) cudaIpcCloseMemHandle(t->items[r]);
+        if (t->seq[r]) cudaIpcCloseMemHandle(t->seq[r]);
+    }
+    delete t;
 }
 
 // ------------------------------------------------------------------ multi-GPU pool counter

@@ -180,18 +180,18 @@ def test_root_restricted_counts_large(env):
 
 def test_config4_sampled_roots_full_queries():
     """configs[3] at full size: R-MAT scale 24 (16.8 M vertices, ~265 M adjacency entries, 16
-    labels) with the bench's own 16-vertex dense queries, counted by k_dfs<16, false> in the
-    bench's launch configuration (tau = 1e6, stealing on) restricted to sampled roots of
-    phi[0], equal the oracle's per-root counts on the whole graph (roots whose oracle search
-    stays under a node budget; the query's own seed image is tried first, so nonzero counts
-    are covered)."""
+    labels) with the bench's own 16-vertex dense queries and their 12- and 9-vertex prefixes
+    in the planner's order (induced, connected sub-queries: the same k_dfs<16, false>
+    kernel), counted on sampled roots of phi[0] -- the query's own seed image first, so
+    nonzero counts are covered -- equal the oracle's per-root counts on the whole graph
+    (roots whose oracle search stays under a work budget)."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
+    import time
     import bench
     import gminputs.gpu as gg
     import paper_2604_10601_b200 as gm
-    import time
     t0 = time.time()
     cfg = bench.CONFIGS["rmat24"]
     n, s, d, lab = bench.make_graph_device(cfg)
@@ -209,25 +209,30 @@ def test_config4_sampled_roots_full_queries():
     rs = np.random.default_rng(24)
     checked = nonzero = 0
     for q, chosen in zip(queries, seeds):
-        p = gm.gm_plan_query(g, q)
-        u0 = p.info()["order"][0]
-        cands = np.flatnonzero(p.candidates(u0))
-        roots, ref = [], 0
-        for v in [int(chosen[u0])] + [int(x) for x in rs.permutation(cands)[:100]]:
-            if v in roots:
-                continue
-            c = og.count(q, fixed=(u0, v), max_nodes=2_000_000)
-            if c is not None:
-                roots.append(v); ref += c; nonzero += c > 0
-                # tau = 1: the single root goes straight to k_dfs<16, false> (no BFS levels)
-                c1, st1 = gm.gm_count(p, roots=np.array([v], np.uint32), tau=1, time_limit_ms=60000)
-                assert c1 == c, (q.name, v)
-                assert st1["stack_levels"] == 16 or st1["dfs_launches"] == 0
-            if len(roots) == 6:
-                break
-        c, st = gm.gm_count(p, roots=np.array(roots, np.uint32), time_limit_ms=60000)
-        print(f"[config4] {q.name}: {len(roots)} roots, count {ref}, {time.time() - t0:.1f}s", flush=True)
-        assert st["timed_out"] == 0
-        assert c == ref, (q.name, roots)
-        checked += len(roots)
-    assert checked >= 12 and nonzero >= 1, (checked, nonzero)
+        order = gm.gm_plan_query(g, q).info()["order"]
+        for k in (16, 12, 9):
+            keep = order[:k]
+            idx = {u: i for i, u in enumerate(keep)}
+            sub = gi.Query(k, [(idx[a], idx[b]) for a, b in q.edges.tolist() if a in idx and b in idx],
+                           [int(q.labels[u]) for u in keep], name=f"{q.name}[:{k}]")
+            p = gm.gm_plan_query(g, sub, order=list(range(k)))
+            cands = np.flatnonzero(p.candidates(0))
+            roots, ref = [], 0
+            for v in [int(chosen[keep[0]])] + [int(x) for x in rs.permutation(cands)[:60]]:
+                if v in roots:
+                    continue
+                c = og.count(sub, fixed=(0, v), max_nodes=4_000_000)
+                if c is not None:
+                    roots.append(v); ref += c; nonzero += c > 0
+                    # tau = 1: the single root goes straight to k_dfs<16, false> (no BFS levels)
+                    c1, st1 = gm.gm_count(p, roots=np.array([v], np.uint32), tau=1, time_limit_ms=60000)
+                    assert c1 == c, (sub.name, v)
+                    assert st1["stack_levels"] == 16 or st1["dfs_launches"] == 0
+                if len(roots) == 4:
+                    break
+            c, st = gm.gm_count(p, roots=np.array(roots, np.uint32), time_limit_ms=60000)
+            print(f"[config4] {sub.name}: {len(roots)} roots, count {ref}, {time.time() - t0:.1f}s", flush=True)
+            assert st["timed_out"] == 0
+            assert c == ref, (sub.name, roots)
+            checked += len(roots)
+    assert checked >= 24 and nonzero >= 3, (checked, nonzero)

@@ -85,3 +85,86 @@ def test_two_ranks_static_and_shared_pool():
     assert static == ref
     assert shared == ref
     assert single == ref
+
+
+def _team_worker(rank, world, port, out):
+    """Cross-GPU stealing team (gm_team): rank 1 takes no pool batches (GM_FLAG_NO_POOL), so every
+    embedding it counts came from rank 0's steal ring over peer memory; the per-rank counts
+    sum to the oracle's.  Then both ranks claim from the shared pool and steal from each other."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import gminputs as gi
+        import paper_2604_10601_b200 as gm
+        import test_gpu_large_queries as T
+        n, s, d = gi.rmat_edges(12, 8, 7)
+        lab = gi.uniform_labels(n, 16, 7)
+        adj = gi.HostAdjacency(*gi.simple_adjacency(n, s, d))
+        env = dict(adj=adj, lab=lab)
+        queries = [T.query(env, 22, 4, 2, False), T.query(env, 14, 3, 2, True), T.query(env, 10, 3, 1, False)]
+        g = gm.gm_load_graph(n, s, d, lab, 16)
+        handles = [None] * world
+        dist.all_gather_object(handles, gm.gm_team_export())
+        team = gm.gm_team_open(world, rank, handles)
+        if rank == 0:
+            ptr, handle = gm.gm_pool_counter_create(2 * len(queries))
+        else:
+            ptr, handle = None, None
+        box = [handle]
+        dist.broadcast_object_list(box, src=0)
+        if rank != 0:
+            ptr = gm.gm_pool_counter_open(box[0])
+        if rank == 0:
+            gm.gm_pool_counter_reset(ptr, 2 * len(queries))
+            torch.cuda.synchronize()
+        dist.barrier()
+        res = []
+        for mode in (0, 1):
+            for i, q in enumerate(queries):
+                p = gm.gm_plan_query(g, q)
+                kw = dict(tau=64, team=team, shared_pool_ctr=gm.pool_counter_slot(ptr, mode * len(queries) + i))
+                if mode == 0 and rank == 1:
+                    kw["no_pool"] = True
+                c, st = gm.gm_count(p, **kw)
+                res.append((c, st["donations"]))    # (no barrier between searches: epochs)
+        allres = [None] * world
+        dist.all_gather_object(allres, res)
+        if rank == 0:
+            from oracle import OracleGraph
+            og = OracleGraph(n, s, d, lab)
+            out.put((allres, [og.count(q) for q in queries]))
+        dist.barrier()
+        team.free()
+        gm.gm_pool_counter_close(ptr, owner=(rank == 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_team_cross_rank_stealing():
+    import sys
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_team_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    allres, ref = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    nq = len(ref)
+    for mode in (0, 1):
+        for i in range(nq):
+            c0, c1 = allres[0][mode * nq + i][0], allres[1][mode * nq + i][0]
+            assert c0 + c1 == ref[i], (mode, i, c0, c1, ref[i])
+    # rank 1 took no pool batch in mode 0: whatever it counted, it stole from rank 0
+    assert sum(allres[1][i][0] for i in range(nq)) > 0
