@@ -91,6 +91,10 @@ typedef struct {
     uint64_t device_bytes; /* device memory held by the graph */
     uint32_t hubs;         /* vertices with a hub adjacency bitmap (gm_graph_build_hubs) */
     uint32_t hub_min_degree;
+    uint64_t hub_bytes;    /* device bytes of the hub index (bitmaps + summary rows) */
+    uint32_t hub_summary_words; /* words per hub summary row (1 bit per 256 vertices); 0 when the
+                                   index fits in L2 and has no summary level */
+    uint32_t reserved;
 } gm_graph_info_t;
 
 GM_API int gm_graph_info(const gm_graph *g, gm_graph_info_t *info);
@@ -99,13 +103,18 @@ GM_API int gm_graph_info(const gm_graph *g, gm_graph_info_t *info);
  * gm_graph_build_hubs -- (re)build the hub adjacency index: for the highest-degree
  * vertices (degree >= min_degree, at most budget_bytes / (4*ceil(n/32)) of them) a bitmap
  * of N(v) over all vertex ids, used by the search to test v in N(w) with one word read
- * instead of a binary search.  gm_load_graph builds it with
+ * instead of a binary search.  An index larger than the L2 cache
+ * also gets a summary level: one bit per 256-vertex block of each bitmap (set iff the block
+ * holds a neighbour), so most failing tests read an L2-resident summary word instead of a
+ * DRAM sector of the bitmap.  summary: -1 = that rule (gm_load_graph's choice), 0 = never,
+ * 1 = always.  gm_load_graph builds it with
  * min_degree 64 and a 64 MiB budget when the CSR fits in L2 beside it, else an 8 GiB budget
  * (at most a quarter of the free device memory); budget_bytes = 0 removes it.  Results
  * never depend on it.
  * Synchronizes `stream`.  Do not call while a search on this graph is running.
  */
-GM_API int gm_graph_build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, void *stream);
+GM_API int gm_graph_build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, int summary,
+                               void *stream);
 
 /*
  * gm_graph_export -- copy the CSR back to host buffers (tests, debugging).

@@ -74,9 +74,11 @@ class Graph:
         L.check(L.lib().gm_graph_info(self._h, ctypes.byref(inf)))
         return {k: getattr(inf, k) for k, _ in inf._fields_}
 
-    def build_hubs(self, budget_bytes=64 << 20, min_degree=64, stream=None):
-        """Rebuild the hub adjacency index (budget 0 removes it)."""
-        L.check(L.lib().gm_graph_build_hubs(self._h, int(budget_bytes), int(min_degree), _stream_handle(stream)))
+    def build_hubs(self, budget_bytes=64 << 20, min_degree=64, summary=-1, stream=None):
+        """Rebuild the hub adjacency index (budget 0 removes it); summary level: -1 when the
+        index exceeds L2, 0 never, 1 always."""
+        L.check(L.lib().gm_graph_build_hubs(self._h, int(budget_bytes), int(min_degree), int(summary),
+                                            _stream_handle(stream)))
 
     def export(self):
         """(offs, nbr, labels) copied to host numpy arrays."""

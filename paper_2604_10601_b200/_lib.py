@@ -42,7 +42,8 @@ GM_POOL_COUNTER_STRIDE = 128
 class GraphInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_uint64), ("num_adj", ctypes.c_uint64), ("num_labels", ctypes.c_uint32),
                 ("d_max", ctypes.c_uint32), ("device_bytes", ctypes.c_uint64), ("hubs", ctypes.c_uint32),
-                ("hub_min_degree", ctypes.c_uint32)]
+                ("hub_min_degree", ctypes.c_uint32), ("hub_bytes", ctypes.c_uint64),
+                ("hub_summary_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -90,7 +91,7 @@ def lib():
                                     ctypes.POINTER(vp)]
         L.gm_graph_info.argtypes = [vp, ctypes.POINTER(GraphInfo)]
         L.gm_graph_export.argtypes = [vp, vp, vp, vp]
-        L.gm_graph_build_hubs.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, vp]
+        L.gm_graph_build_hubs.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, vp]
         L.gm_free_graph.argtypes = [vp]
         L.gm_free_graph.restype = None
         L.gm_plan_query.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p, u32p, ctypes.c_uint32, vp,

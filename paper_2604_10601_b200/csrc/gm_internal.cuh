@@ -55,10 +55,14 @@ struct gm_graph {
     uint32_t hub_min_degree = 0;
     uint32_t hub_words = 0;        // ceil(n/32) words per hub bitmap
     uint32_t *hub_bits = nullptr;  // nhubs * hub_words
+    // two-level index for indexes larger than L2 (hubs.cu): bit b of hub h's summary row is 1
+    // iff its bitmap has a set bit among vertices [256 b, 256 b + 256) (one 32-byte sector)
+    uint32_t summ_words = 0;       // ceil(n / 8192) words per summary row; 0: no summary
+    uint32_t *hub_summ = nullptr;  // nhubs * summ_words
 };
 
 namespace gm {
-int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, cudaStream_t st);
+int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, int summary, cudaStream_t st);
 void free_hubs(gm_graph *g);
 constexpr uint64_t kDefaultHubBudget = 64ull << 20;   // fits beside the graph in the 126 MB L2
 constexpr uint64_t kLargeHubBudget = 8ull << 30;     // graphs whose CSR cannot stay in L2

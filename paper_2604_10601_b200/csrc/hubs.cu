@@ -10,6 +10,7 @@
 // by a byte budget sized to stay L2-resident beside the CSR.  Lists of non-hubs are still
 // binary searched.  (an index the paper does not use; BEEP's
 // per-centre adjacency matrix, §6.2, is its closest relative.)
+#include <algorithm>
 #include <vector>
 
 #include "gm_internal.cuh"
@@ -25,6 +26,28 @@ __global__ void k_hub_bits(uint32_t S, const uint32_t *__restrict__ offs, const 
     for (uint32_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
         const uint32_t w = nbr[e];
         atomicOr(row + (w >> 5), 1u << (w & 31));
+    }
+}
+
+// Summary rows: thread j of hub h reads the 32-byte sector j of the bitmap (vertices
+// [256 j, 256 j + 256)), and a warp's ballot over 32 consecutive sectors is summary word j/32.
+__global__ void k_hub_summ(uint32_t nhubs, uint32_t words, uint32_t summ_words, const uint32_t *__restrict__ bits,
+                           uint32_t *__restrict__ summ) {
+    const uint64_t sectors = (uint64_t)summ_words * 32;
+    const uint64_t total = (uint64_t)nhubs * sectors;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        bool any = false;
+        if (i < total) {
+            const uint64_t h = i / sectors, j = i % sectors;
+            const uint32_t *row = bits + h * words;
+            for (uint32_t k = 0; k < 8; ++k) {
+                const uint64_t w = j * 8 + k;
+                if (w < words) any = any || row[w] != 0;
+            }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, any);
+        if ((threadIdx.x & 31) == 0 && i < total) summ[i / 32] = m;   // sectors is a multiple of 32
     }
 }
 
@@ -45,11 +68,14 @@ uint64_t default_hub_budget(const gm_graph *g) {
 
 void free_hubs(gm_graph *g) {
     cudaFree(g->hub_bits);
+    cudaFree(g->hub_summ);
     g->hub_bits = nullptr;
+    g->hub_summ = nullptr;
+    g->summ_words = 0;
     g->nhubs = 0;
 }
 
-int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, cudaStream_t st) {
+int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, int summary, cudaStream_t st) {
     free_hubs(g);
     g->hub_min_degree = min_degree;
     g->hub_words = (uint32_t)((g->n + 31) / 32);
@@ -70,6 +96,21 @@ int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, cudaStre
     GM_CK(cudaMemsetAsync(g->hub_bits, 0, per_hub * k, st));
     k_hub_bits<<<k, 256, 0, st>>>(g->S, g->offs, g->nbr, g->hub_words, g->hub_bits);
     GM_CK(cudaGetLastError());
+    // An index larger than L2 gets a summary level (1 bit per 32-byte bitmap sector, 1/256 of
+    // the index): a test whose summary bit is 0 -- most tests fail, and a hub of degree d has
+    // neighbours in about d of the n/256 blocks -- is answered from the L2-resident summary
+    // instead of a DRAM sector of the bitmap.
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    if (summary > 0 || (summary < 0 && per_hub * k > (uint64_t)l2)) {
+        g->summ_words = (uint32_t)((g->n + 8191) / 8192);
+        GM_CK(cudaMalloc(&g->hub_summ, 4ull * g->summ_words * k));
+        const uint64_t threads = (uint64_t)k * g->summ_words * 32;
+        const uint64_t blocks = std::min<uint64_t>((threads + 255) / 256, 148ull * 32);
+        k_hub_summ<<<(unsigned)blocks, 256, 0, st>>>(k, g->hub_words, g->summ_words, g->hub_bits, g->hub_summ);
+        GM_CK(cudaGetLastError());
+    }
     GM_CK(cudaStreamSynchronize(st));
     g->nhubs = k;
     return GM_OK;
@@ -77,8 +118,9 @@ int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, cudaStre
 
 }  // namespace gm
 
-extern "C" int gm_graph_build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, void *stream) {
+extern "C" int gm_graph_build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, int summary,
+                                   void *stream) {
     gm::set_error("");
     GM_REQ(g, GM_ERR_ARG, "gm_graph_build_hubs: NULL graph");
-    return gm::build_hubs(g, budget_bytes, min_degree, (cudaStream_t)stream);
+    return gm::build_hubs(g, budget_bytes, min_degree, summary, (cudaStream_t)stream);
 }

@@ -64,6 +64,9 @@ constexpr uint32_t FULL = 0xffffffffu;
 #define GM_MINB32 9
 #endif
 #define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? GM_MINB16 : GM_MINB32))
+#ifndef GM_HUB_SUMMARY
+#define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
+#endif
 #ifndef GM_TWO_VEC
 #define GM_TWO_VEC 1       // pair-counting intersection: 128-element rounds with 16-byte loads
 #endif
@@ -124,6 +127,8 @@ struct SearchParams {
     unsigned long long *q_seq;  // q_cap per-slot sequence numbers (Vyukov bounded MPMC ring)
     unsigned long long q_cap;
     const uint32_t *__restrict__ hub_bits;  // hub bitmaps (row w for device ids w < nhubs)
+    const uint32_t *__restrict__ hub_summ;  // summary rows (1 bit per 256 vertices), or NULL
+    uint32_t summ_words;
     uint32_t nhubs;                         // 0: no hub index
     uint32_t hub_words;
     const uint32_t *__restrict__ new2old;   // device id -> original id (enumerate output)
@@ -203,6 +208,26 @@ __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint
     return (ld_nc(P.cand + P.candoff[l] + (v >> 5)) >> (v & 31)) & 1u;
 }
 
+// Summary bit of hub h for vertex x: 0 means no neighbour of h in x's 256-vertex block
+// (so x is not one); always 1 without a summary level.
+__device__ __forceinline__ uint32_t hub_summ_word(const SearchParams &P, uint32_t h, uint32_t x, uint32_t &words) {
+#if GM_HUB_SUMMARY
+    if (P.hub_summ) {
+        ++words;
+        return ld_nc(P.hub_summ + (unsigned long long)h * P.summ_words + (x >> 13));
+    }
+#endif
+    return 0xffffffffu;
+}
+__device__ __forceinline__ bool summ_says(uint32_t sw, uint32_t x) { return (sw >> ((x >> 8) & 31)) & 1u; }
+
+// x in N(h) for a hub h: the summary word (if any), then the bitmap word
+__device__ __forceinline__ bool hub_bit(const SearchParams &P, uint32_t h, uint32_t x, uint32_t &words) {
+    if (!summ_says(hub_summ_word(P, h, x, words), x)) return false;
+    ++words;
+    return (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+}
+
 // Is {a, b} an edge?  la = L(a), lb = L(b).  The test is symmetric (b in N_lb(a) iff a in
 // N_la(b)), so it takes the cheapest side: the hub bitmap of a or of b if either is a hub
 // (device ids are ordered by degree: "is a hub" is w < nhubs), else a binary search of the
@@ -211,8 +236,7 @@ __device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t a, uint
                                          uint32_t &words) {
     if (a < P.nhubs || b < P.nhubs) {
         const uint32_t h = a < P.nhubs ? a : b, x = a < P.nhubs ? b : a;
-        ++words;
-        return (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+        return hub_bit(P, h, x, words);
     }
     const uint32_t r = a > b ? a : b, x = a > b ? b : a, lx = a > b ? lb : la;
     const uint32_t row = r * P.S + lx;
@@ -418,25 +442,38 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     constexpr int G = D <= 8 ? 2 : GM_PROBES_WIDE;
     for (int c = 0; c < nchk; c += G) {
         if (!__any_sync(FULL, ok)) break;
-        uint32_t w[G], b[G], n[G];
-        bool r[G], need[G];
+        uint32_t w[G], b[G], n[G], hh[G], hx[G], sw[G];
+        bool r[G], need[G], hub[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const bool act = ok && c + g < nchk;
             w[g] = act ? CHK(c + g, ccol) : 0u;
-            r[g] = true; need[g] = false; b[g] = 0; n[g] = 0;
+            r[g] = true; need[g] = false; hub[g] = false; b[g] = 0; n[g] = 0; hh[g] = 0; hx[g] = 0;
+            sw[g] = 0xffffffffu;
             if (act) {
                 // hub bitmap of w, or of v (the test is symmetric), else binary search of w's row
                 if (w[g] < P.nhubs || (GM_VHUB && v < P.nhubs)) {
-                    const uint32_t h = w[g] < P.nhubs ? w[g] : v, x = w[g] < P.nhubs ? v : w[g];
-                    r[g] = (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
-                    ++words;
+                    hh[g] = w[g] < P.nhubs ? w[g] : v;
+                    hx[g] = w[g] < P.nhubs ? v : w[g];
+                    hub[g] = true;
+                    sw[g] = hub_summ_word(P, hh[g], hx[g], words);   // (summary level: first load)
                 } else {
                     const uint32_t row = w[g] * P.S + lab;
                     b[g] = ld_nc(P.offs + row);
                     n[g] = ld_nc(P.offs + row + 1) - b[g];
                     need[g] = true;
                     words += 2;
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {       // bitmap words, only where the summary bit is set
+            if (hub[g]) {
+                if (summ_says(sw[g], hx[g])) {
+                    ++words;
+                    r[g] = (ld_nc(P.hub_bits + (unsigned long long)hh[g] * P.hub_words + (hx[g] >> 5)) >> (hx[g] & 31)) & 1u;
+                } else {
+                    r[g] = false;
                 }
             }
         }
@@ -731,10 +768,14 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                         const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
                         uint32_t wv[4];
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) wv[g] = hit[g] ? ld_nc(row + (x[g] >> 5)) : 0u;
+                        for (int g = 0; g < 4; ++g) wv[g] = hit[g] ? hub_summ_word(P, f_gown, x[g], words) : 0u;
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            hit[g] = hit[g] && summ_says(wv[g], x[g]);
+                            if (hit[g]) { wv[g] = ld_nc(row + (x[g] >> 5)); ++words; }
+                        }
 #pragma unroll
                         for (int g = 0; g < 4; ++g) hit[g] = hit[g] && ((wv[g] >> (x[g] & 31)) & 1u);
-                        words += nval;
                     } else {
                         // four lower bounds in the same list: the trip count is warp-uniform
                         uint32_t n = f_ge - f_gb, b[4] = {f_gb, f_gb, f_gb, f_gb};
@@ -769,12 +810,15 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     words += step >> 5;
                     bool hit, hit2 = false;
                     if (f_gown < P.nhubs) {
-                        words += step >> 5;
                         const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
-                        const uint32_t w1 = ld_nc(row + (x >> 5));
-                        const uint32_t w2 = step == 64 ? ld_nc(row + (x2 >> 5)) : 0u;
+                        const uint32_t s1 = hub_summ_word(P, f_gown, x, words);
+                        const uint32_t s2 = step == 64 ? hub_summ_word(P, f_gown, x2, words) : 0u;
+                        const bool p1 = summ_says(s1, x), p2 = step == 64 && summ_says(s2, x2);
+                        const uint32_t w1 = p1 ? ld_nc(row + (x >> 5)) : 0u;
+                        const uint32_t w2 = p2 ? ld_nc(row + (x2 >> 5)) : 0u;
+                        words += p1 + p2;
                         hit = (w1 >> (x & 31)) & 1u;
-                        hit2 = step == 64 && ((w2 >> (x2 & 31)) & 1u);
+                        hit2 = (w2 >> (x2 & 31)) & 1u;
                     } else {
                         hit = contains(P.nbr, f_gb, f_ge, x, words);
                         if (step == 64) hit2 = contains(P.nbr, f_gb, f_ge, x2, words);
@@ -816,8 +860,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     ++words;
                     bool hit;
                     if (s_gown < P.nhubs) {
-                        ++words;
-                        hit = (ld_nc(P.hub_bits + (unsigned long long)s_gown * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
+                        hit = hub_bit(P, s_gown, x, words);
                     } else {
                         hit = contains(P.nbr, s_gb, s_ge, x, words);
                     }
@@ -1547,6 +1590,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     P.nhubs = g->nhubs;
     P.hub_bits = g->hub_bits;
     P.hub_words = g->hub_words;
+    P.hub_summ = g->hub_summ;
+    P.summ_words = g->summ_words;
     P.new2old = g->new2old;
     P.old2new = g->old2new;
     if (!W.ctrl) GM_CK(cudaMalloc(&W.ctrl, sizeof(Ctrl)));

@@ -236,3 +236,20 @@ def test_config4_sampled_roots_full_queries():
             assert c == ref, (sub.name, roots)
             checked += len(roots)
     assert checked >= 24 and nonzero >= 3, (checked, nonzero)
+
+
+@pytest.mark.parametrize("k,seed,leaves,same", [(10, 3, 2, True), (14, 4, 2, False), (22, 4, 2, True), (30, 2, 1, False),
+                                                (16, 3, 0, False), (32, 3, 0, False)])
+def test_two_level_hub_index(env, k, seed, leaves, same):
+    """The hub index's summary level (1 bit per 256-vertex block, used by default only when the
+    index exceeds L2) forced on, with every vertex of degree >= 2 a hub: counts at D=16/32 on
+    every counting path equal the oracle's; then the default index is restored."""
+    gm = env["gm"]
+    q = query(env, k, seed, leaves, same)
+    g = env["g"]
+    g.build_hubs(64 << 20, 2, 1)
+    try:
+        assert g.info()["hub_summary_words"] > 0
+        check_all_paths(env, q)
+    finally:
+        g.build_hubs(64 << 20, 64, -1)

@@ -204,8 +204,8 @@ def test_pair_count_two_leaves(gm, seed):
     g = gm.gm_load_graph(n, s, d, lab, nl)
     ref = og.count(q)
     order = list(range(k))                         # the two leaves last
-    for budget, mindeg in ((64 << 20, 2), (64 << 20, 64), (0, 64)):
-        g.build_hubs(budget, mindeg)
+    for budget, mindeg, summ in ((64 << 20, 2, 0), (64 << 20, 2, 1), (64 << 20, 64, -1), (0, 64, -1)):
+        g.build_hubs(budget, mindeg, summ)
         p = gm.gm_plan_query(g, q, order=order)
         for tau in (1, 10 ** 6):
             assert gm.gm_count(p, tau=tau)[0] == ref
@@ -505,8 +505,9 @@ def test_hub_index_does_not_change_results(gm, seed):
     g = gm.gm_load_graph(n, s, d, lab, nl)
     ref = og.count(q)
     assert g.info()["hubs"] > 0
-    for budget, mindeg in ((64 << 20, 2), (0, 64), (64 << 20, 64)):
-        g.build_hubs(budget, mindeg)
+    for budget, mindeg, summ in ((64 << 20, 2, 0), (64 << 20, 2, 1), (0, 64, -1), (64 << 20, 64, -1)):
+        g.build_hubs(budget, mindeg, summ)
+        assert (g.info()["hub_summary_words"] > 0) == (summ == 1 and budget > 0)
         if budget == 0:
             assert g.info()["hubs"] == 0
         p = gm.gm_plan_query(g, q)
@@ -689,8 +690,8 @@ def test_pair_count_long_lists_closed_form(gm):
     assert deg.max() >= 512                      # hub lists: many 128-element rounds
     g = gm.gm_load_graph(n, s, d)
     q = gi.Query(4, [(0, 1), (1, 2), (2, 3)], [0, 0, 0, 0])
-    for budget, mindeg in ((64 << 20, 64), (0, 64)):       # hub bitmaps / binary search only
-        g.build_hubs(budget, mindeg)
+    for budget, mindeg, summ in ((64 << 20, 64, 0), (64 << 20, 64, 1), (0, 64, -1)):   # bitmaps / + summary / search
+        g.build_hubs(budget, mindeg, summ)
         p = gm.gm_plan_query(g, q, order=[1, 2, 0, 3])
         for tau in (1, 10 ** 6):
             c, st = gm.gm_count(p, tau=tau, symmetry=False)

@@ -18,6 +18,12 @@ run() {  # cfg nroots limit qi...
     done
   done
 }
-run rmat18 0 300 4 5 6 7 > $OUT/ab_rmat18_pair.log 2>&1
-run rmat18 100 0 0 1 2 3 > $OUT/ab_rmat18_dense.log 2>&1
-run rmat24 0 1000 0 1 2 3 > $OUT/ab_rmat24.log 2>&1
+SETS=${AB_SETS:-"pair dense r24"}
+for set in $SETS; do
+  case $set in
+    pair)  run rmat18 0 300 4 5 6 7 > $OUT/ab_rmat18_pair.log 2>&1 ;;
+    dense) run rmat18 100 0 0 1 2 3 > $OUT/ab_rmat18_dense.log 2>&1 ;;
+    r24)   run rmat24 0 1000 0 1 2 3 > $OUT/ab_rmat24.log 2>&1 ;;
+    r26)   run rmat26 0 1000 0 1 2 3 > $OUT/ab_rmat26.log 2>&1 ;;
+  esac
+done

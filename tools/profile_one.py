@@ -36,7 +36,8 @@ else:
               open(cache, "w"))
 g = gm.gm_load_graph(n, s, d, lab, cfg["labels"])
 if os.environ.get("GM_HUB_MB"):                 # hub-index sweeps
-    g.build_hubs(int(float(os.environ["GM_HUB_MB"]) * (1 << 20)), int(os.environ.get("GM_HUB_MIN", "64")))
+    g.build_hubs(int(float(os.environ["GM_HUB_MB"]) * (1 << 20)), int(os.environ.get("GM_HUB_MIN", "64")),
+                 int(os.environ.get("GM_HUB_SUMM", "-1")))
 q = qs[qi]
 p = gm.gm_plan_query(g, q)
 u0 = p.info()["order"][0]
