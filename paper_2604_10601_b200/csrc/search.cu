@@ -71,8 +71,8 @@ constexpr uint32_t FULL = 0xffffffffu;
 #define GM_TWO_VEC 1       // pair-counting intersection: 128-element rounds with 16-byte loads
 #endif
 #ifndef GM_PROBES_WIDE
-#define GM_PROBES_WIDE 2   // probes in flight per lane in the 16/32-level kernels (process()); 4 was
-#endif                     // measured 13-51 % fewer tasks/s on rmat24 (wasted probes)
+#define GM_PROBES_WIDE 1   // checks per pass in the 16/32-level kernels (process()): on rmat24 1 beat
+#endif                     // 2 by 3-15 % and 4 lost 13-51 % tasks/s (wasted DRAM probes)
 constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
 constexpr uint32_t kItemWords = 6 + kMaxQ;     // [depth, cb, cl, cs, home, epoch, prefix[kMaxQ]]
 constexpr uint32_t kMaxTeam = 8;               // ranks of a stealing team (gm_team)
@@ -435,10 +435,10 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
     // G checks per pass: their hub-id, bitmap/row-offset and binary-search loads are
-    // independent, so each lane keeps G dependent-load chains in flight (ncu: the kernel is
-    // bound by long-scoreboard stalls on its probes, not by bandwidth).  A larger G wastes the
-    // probes of tasks that fail an earlier check of the group (most do): G = 4 in the 16/32-level
-    // kernels cost 13-51 % of rmat24's tasks/s, so G = 2 everywhere by default.
+    // independent, so each lane keeps G dependent-load chains in flight (the L2-resident
+    // 8-level kernel is bound by long-scoreboard stalls on its probes: G = 2).  A larger G
+    // wastes the probes of tasks that fail an earlier check of the group (most do), which on
+    // the DRAM-resident configs costs more than the overlap gains: G = 1 for 16/32 levels.
     constexpr int G = D <= 8 ? 2 : GM_PROBES_WIDE;
     for (int c = 0; c < nchk; c += G) {
         if (!__any_sync(FULL, ok)) break;

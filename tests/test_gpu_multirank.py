@@ -87,10 +87,26 @@ def test_two_ranks_static_and_shared_pool():
     assert single == ref
 
 
+def _p4_closed_form(n, s, d):
+    """4-vertex paths (ordered embeddings of P4) in the simple graph: sum over ordered edges
+    (a, b) of (d_a - 1)(d_b - 1) minus trace(A^3) (tests/test_gpu_parity.py pins it)."""
+    import gminputs as gi
+    import scipy.sparse as sp
+    off, nb = gi.simple_adjacency(n, s, d)
+    deg = np.diff(off).astype(np.int64)
+    rows = np.repeat(np.arange(n), deg)
+    A = sp.csr_matrix((np.ones(len(nb), np.int64), (rows, nb.astype(np.int64))), shape=(n, n))
+    return int(((deg[rows] - 1) * (deg[nb] - 1)).sum()) - int((A @ A).multiply(A).sum())
+
+
 def _team_worker(rank, world, port, out):
-    """Cross-GPU stealing team (gm_team): rank 1 takes no pool batches (GM_FLAG_NO_POOL), so every
-    embedding it counts came from rank 0's steal ring over peer memory; the per-rank counts
-    sum to the oracle's.  Then both ranks claim from the shared pool and steal from each other."""
+    """Cross-GPU stealing team (gm_team): in mode 0 rank 1 takes no pool batches
+    (GM_FLAG_NO_POOL), so every embedding it counts came from rank 0's steal ring over peer
+    memory; in mode 1 both ranks claim from the shared pool and steal from each other.  The
+    per-rank counts sum to the closed form.  The work is made long (every embedding of P4
+    validated task by task: set/pair counting and symmetry breaking off) because two
+    processes on ONE GPU time-slice it: rank 1's warps run while rank 0's are parked with
+    items in its ring."""
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -100,18 +116,14 @@ def _team_worker(rank, world, port, out):
     try:
         import gminputs as gi
         import paper_2604_10601_b200 as gm
-        import test_gpu_large_queries as T
-        n, s, d = gi.rmat_edges(12, 8, 7)
-        lab = gi.uniform_labels(n, 16, 7)
-        adj = gi.HostAdjacency(*gi.simple_adjacency(n, s, d))
-        env = dict(adj=adj, lab=lab)
-        queries = [T.query(env, 22, 4, 2, False), T.query(env, 14, 3, 2, True), T.query(env, 10, 3, 1, False)]
-        g = gm.gm_load_graph(n, s, d, lab, 16)
+        n, s, d = gi.rmat_edges(13, 16, 77)
+        g = gm.gm_load_graph(n, s, d)
+        q = gi.Query(4, [(0, 1), (1, 2), (2, 3)], [0, 0, 0, 0])
         handles = [None] * world
         dist.all_gather_object(handles, gm.gm_team_export())
         team = gm.gm_team_open(world, rank, handles)
         if rank == 0:
-            ptr, handle = gm.gm_pool_counter_create(2 * len(queries))
+            ptr, handle = gm.gm_pool_counter_create(4)
         else:
             ptr, handle = None, None
         box = [handle]
@@ -119,24 +131,22 @@ def _team_worker(rank, world, port, out):
         if rank != 0:
             ptr = gm.gm_pool_counter_open(box[0])
         if rank == 0:
-            gm.gm_pool_counter_reset(ptr, 2 * len(queries))
+            gm.gm_pool_counter_reset(ptr, 4)
             torch.cuda.synchronize()
         dist.barrier()
         res = []
+        p = gm.gm_plan_query(g, q, order=[1, 2, 0, 3])
         for mode in (0, 1):
-            for i, q in enumerate(queries):
-                p = gm.gm_plan_query(g, q)
-                kw = dict(tau=64, team=team, shared_pool_ctr=gm.pool_counter_slot(ptr, mode * len(queries) + i))
-                if mode == 0 and rank == 1:
-                    kw["no_pool"] = True
-                c, st = gm.gm_count(p, **kw)
-                res.append((c, st["donations"]))    # (no barrier between searches: epochs)
+            kw = dict(tau=4096, team=team, shared_pool_ctr=gm.pool_counter_slot(ptr, mode), set_count=False,
+                      pair_count=False, symmetry=False)
+            if mode == 0 and rank == 1:
+                kw["no_pool"] = True
+            c, st = gm.gm_count(p, **kw)
+            res.append((c, st["donations"], st["tasks"]))     # (no barrier between searches: epochs)
         allres = [None] * world
         dist.all_gather_object(allres, res)
         if rank == 0:
-            from oracle import OracleGraph
-            og = OracleGraph(n, s, d, lab)
-            out.put((allres, [og.count(q) for q in queries]))
+            out.put((allres, _p4_closed_form(n, s, d)))
         dist.barrier()
         team.free()
         gm.gm_pool_counter_close(ptr, owner=(rank == 0))
@@ -145,12 +155,10 @@ def _team_worker(rank, world, port, out):
 
 
 def test_two_rank_team_cross_rank_stealing():
-    import sys
     import torch
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -161,10 +169,8 @@ def test_two_rank_team_cross_rank_stealing():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    nq = len(ref)
     for mode in (0, 1):
-        for i in range(nq):
-            c0, c1 = allres[0][mode * nq + i][0], allres[1][mode * nq + i][0]
-            assert c0 + c1 == ref[i], (mode, i, c0, c1, ref[i])
-    # rank 1 took no pool batch in mode 0: whatever it counted, it stole from rank 0
-    assert sum(allres[1][i][0] for i in range(nq)) > 0
+        c0, c1 = allres[0][mode][0], allres[1][mode][0]
+        assert c0 + c1 == ref, (mode, c0, c1, ref)
+    # rank 1 took no pool batch in mode 0: whatever it counted, it stole from rank 0's ring
+    assert allres[1][0][0] > 0 and allres[1][0][2] > 0, allres
