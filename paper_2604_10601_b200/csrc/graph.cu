@@ -232,7 +232,8 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
         }
         g->nadj = nsel;
         STEP(cudaMalloc(&g->offs, sizeof(uint32_t) * (rows + 1)));
-        STEP(cudaMalloc(&g->nbr, sizeof(uint32_t) * (nsel ? nsel : 1)));
+        // (+4 words: 16-byte vector and bulk copies of a row may round its end up to 16 bytes)
+        STEP(cudaMalloc(&g->nbr, sizeof(uint32_t) * (nsel + 4)));
         k_offsets<<<grid_for(nsel + 1), 256, 0, st>>>(nsel, k0, rows, g->offs, g->nbr);
         STEP(cudaGetLastError());
         unsigned *d_dmax = (unsigned *)d_bad;

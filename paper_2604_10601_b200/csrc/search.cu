@@ -58,12 +58,18 @@ constexpr uint32_t FULL = 0xffffffffu;
 // 16/32-level kernels: the WarpStack (7.8 / 15.6 KB per warp) limits residency to ~6 / ~3 blocks
 // per SM, so they may use the registers that frees
 #ifndef GM_MINB16
-#define GM_MINB16 9
+#define GM_MINB16 7
 #endif
 #ifndef GM_MINB32
-#define GM_MINB32 9
+#define GM_MINB32 7
 #endif
 #define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? GM_MINB16 : GM_MINB32))
+#ifndef GM_TWO_STAGE
+#define GM_TWO_STAGE 0     // pair-count intersection: stage a short non-hub longer list in shared
+#endif                     // memory with cp.async.bulk (TMA) and search it there
+#if GM_TWO_STAGE
+constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows per warp
+#endif
 #ifndef GM_HUB_SUMMARY
 #define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
 #endif
@@ -147,6 +153,7 @@ struct SearchParams {
     uint32_t two_adj6, two_adj7;    // ... whose query vertex is adjacent to phi[b6] / phi[b7]
     uint32_t two_low;           // deepest level count_two's walk visits
     uint32_t two_walk;          // 1: a per-task row (b6 or b7 == last-2) has same-label images below
+    uint32_t two_stage_row;     // GM_TWO_STAGE: first rows_last row of the staging buffer
     uint32_t rows_chk;          // scratch rows for check images (max checks of a task / par-level list)
     uint32_t rows_last;         // scratch rows for set/pair-counting words
     uint32_t warp_stride;       // bytes of shared memory per warp: WarpStack + scratch rows
@@ -210,9 +217,13 @@ __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint
 
 // Summary bit of hub h for vertex x: 0 means no neighbour of h in x's 256-vertex block
 // (so x is not one); always 1 without a summary level.
+// SUMM = false compiles the summary level out: the L2-resident 8-level kernel (small graphs,
+// no summary by default) keeps its register budget; ignoring a summary is always correct
+// (the bitmaps are complete), it only forgoes the shortcut.
+template <bool SUMM = true>
 __device__ __forceinline__ uint32_t hub_summ_word(const SearchParams &P, uint32_t h, uint32_t x, uint32_t &words) {
 #if GM_HUB_SUMMARY
-    if (P.hub_summ) {
+    if (SUMM && P.hub_summ) {
         ++words;
         return ld_nc(P.hub_summ + (unsigned long long)h * P.summ_words + (x >> 13));
     }
@@ -222,8 +233,9 @@ __device__ __forceinline__ uint32_t hub_summ_word(const SearchParams &P, uint32_
 __device__ __forceinline__ bool summ_says(uint32_t sw, uint32_t x) { return (sw >> ((x >> 8) & 31)) & 1u; }
 
 // x in N(h) for a hub h: the summary word (if any), then the bitmap word
+template <bool SUMM = true>
 __device__ __forceinline__ bool hub_bit(const SearchParams &P, uint32_t h, uint32_t x, uint32_t &words) {
-    if (!summ_says(hub_summ_word(P, h, x, words), x)) return false;
+    if (!summ_says(hub_summ_word<SUMM>(P, h, x, words), x)) return false;
     ++words;
     return (ld_nc(P.hub_bits + (unsigned long long)h * P.hub_words + (x >> 5)) >> (x & 31)) & 1u;
 }
@@ -232,11 +244,12 @@ __device__ __forceinline__ bool hub_bit(const SearchParams &P, uint32_t h, uint3
 // N_la(b)), so it takes the cheapest side: the hub bitmap of a or of b if either is a hub
 // (device ids are ordered by degree: "is a hub" is w < nhubs), else a binary search of the
 // row of the LOWER-degree vertex (the larger device id), which is the shorter list.
+template <bool SUMM = true>
 __device__ __forceinline__ bool has_edge(const SearchParams &P, uint32_t a, uint32_t la, uint32_t b, uint32_t lb,
                                          uint32_t &words) {
     if (a < P.nhubs || b < P.nhubs) {
         const uint32_t h = a < P.nhubs ? a : b, x = a < P.nhubs ? b : a;
-        return hub_bit(P, h, x, words);
+        return hub_bit<SUMM>(P, h, x, words);
     }
     const uint32_t r = a > b ? a : b, x = a > b ? b : a, lx = a > b ? lb : la;
     const uint32_t row = r * P.S + lx;
@@ -320,6 +333,27 @@ __device__ __forceinline__ unsigned long long ring_pop(const SearchParams &P, Ct
     return atomicCAS_system(&RC->q_head, pos, pos + 1) == pos ? pos : ~0ull;
 }
 
+// 1-D bulk copy (TMA engine) global -> shared, completing on an mbarrier with a tx count
+__device__ __forceinline__ void mbar_init(unsigned long long *mbar) {
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_stage(uint32_t *dst, const uint32_t *src, uint32_t bytes, unsigned long long *mbar) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst), m = (uint32_t)__cvta_generic_to_shared(mbar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");      // generic reads of the last use first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(src), "r"(bytes), "r"(m) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *mbar, uint32_t parity) {
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(m), "r"(parity) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -327,7 +361,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 template <int D>
-struct WarpStack {
+struct alignas(16) WarpStack {
     uint32_t v[D][32];    // S[l][lane].v   : candidate data vertex of the task in this lane
     uint32_t cb[D][32];   // S[l][lane].C   : begin of the local candidate slice of lane's partial match
     uint32_t cl[D][32];   //                  its length
@@ -339,6 +373,8 @@ struct WarpStack {
     uint32_t lastlb[32];  //               symmetry-breaking bounds of phi[last] from levels < last-1:
     uint32_t lastub[32];  //               its image must lie in [lastlb, lastub)
     uint32_t tacc[32];    // pair counting: per-lane |A n R| accumulators
+    unsigned long long mbar;  // GM_TWO_STAGE: mbarrier of the warp's bulk-copy staging buffer
+    uint32_t home;            // gm_team: lineage rank of the unit this warp holds
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
 };
@@ -456,7 +492,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
                     hh[g] = w[g] < P.nhubs ? w[g] : v;
                     hx[g] = w[g] < P.nhubs ? v : w[g];
                     hub[g] = true;
-                    sw[g] = hub_summ_word(P, hh[g], hx[g], words);   // (summary level: first load)
+                    sw[g] = hub_summ_word<(D > 8)>(P, hh[g], hx[g], words);   // (summary level: first load)
                 } else {
                     const uint32_t row = w[g] * P.S + lab;
                     b[g] = ld_nc(P.offs + row);
@@ -577,7 +613,7 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
                        (uint32_t)__popc(P.last_same & P.last_adj & ((2u << l) - 1));
         words += 2;
         for (int c = 0; c < k; ++c)
-            if (has_edge(P, mb, P.lab[b], LASTW(c, lane), lab, words)) --cnt;
+            if (has_edge<(D > 8)>(P, mb, P.lab[b], LASTW(c, lane), lab, words)) --cnt;
         S.lastlb[lane] = cnt;
     }
 }
@@ -591,7 +627,7 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     const uint32_t lb_lab = P.lab[P.last_b];                       // L(M[b])
     if (!P.last_sb && (int)P.last_b < l) {   // parent-constant part precomputed by prep_last
         uint32_t cnt = S.lastlb[src];
-        if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lb_lab, v, lab, words)) --cnt;
+        if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge<(D > 8)>(P, mb, lb_lab, v, lab, words)) --cnt;
         return cnt;
     }
     const uint32_t row = mb * P.S + lab;
@@ -609,11 +645,11 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
         const uint32_t e = ub != 0xffffffffu ? lower_bound_idx(P.nbr + lo, len, ub, words) : len;
         uint32_t cnt = e > a ? e - a : 0u;
         if (((same >> l) & 1u) && v >= lb && v < ub &&
-            (((P.last_adj >> l) & 1u) || has_edge(P, mb, lb_lab, v, lab, words)))
+            (((P.last_adj >> l) & 1u) || has_edge<(D > 8)>(P, mb, lb_lab, v, lab, words)))
             --cnt;
         for (uint32_t c = 0; c < P.last_k; ++c) {
             const uint32_t w = LASTW(c, src);
-            if (w >= lb && w < ub && has_edge(P, mb, lb_lab, w, lab, words)) --cnt;
+            if (w >= lb && w < ub && has_edge<(D > 8)>(P, mb, lb_lab, w, lab, words)) --cnt;
         }
         for (uint32_t c = 0; c < P.last_ka; ++c) {
             const uint32_t w = LASTW(P.last_k + c, src);
@@ -623,9 +659,9 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     }
     // mapped vertices adjacent to phi[b] in Q lie in the slice for sure (same label)
     uint32_t cnt = hi - lo - (uint32_t)__popc(same & P.last_adj & ((2u << l) - 1));
-    if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge(P, mb, lb_lab, v, lab, words)) --cnt;
+    if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge<(D > 8)>(P, mb, lb_lab, v, lab, words)) --cnt;
     for (uint32_t c = 0; c < P.last_k; ++c)
-        if (has_edge(P, mb, lb_lab, LASTW(c, src), lab, words)) --cnt;
+        if (has_edge<(D > 8)>(P, mb, lb_lab, LASTW(c, src), lab, words)) --cnt;
     return cnt;
 }
 
@@ -665,8 +701,8 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
         for (int i = l - 1; i >= (int)P.two_low; --i) {
             const uint32_t w = S.v[i][p];
             bool a = false, r = false;
-            if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge(P, m6, P.lab[b6], w, lab6, words);
-            if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge(P, m7, P.lab[b7], w, lab7, words);
+            if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], w, lab6, words);
+            if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], w, lab7, words);
             inA += a; inR += r; inAR += a && r;
             p = S.pid[i][p];
         }
@@ -692,7 +728,7 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
 template <int D>
 __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
                                                         uint32_t v, uint32_t src, bool F, uint32_t lane,
-                                                        uint32_t &words) {
+                                                        uint32_t &words, uint32_t &stage_phase) {
     const uint32_t lab6 = P.lab[l + 1], lab7 = P.lab[l + 2];
     const int b6 = (int)P.two_b6, b7 = (int)P.two_b7;
     uint32_t m6 = v, m7 = v, a0 = 0, a1 = 0, r0 = 0, r1 = 0, inA = 0, inR = 0, inAR = 0;
@@ -710,8 +746,8 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
             for (int i = l - 1; i >= (int)P.two_low; --i) {
                 const uint32_t w = S.v[i][p];
                 bool a = false, r = false;
-                if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge(P, m6, P.lab[b6], w, lab6, words);
-                if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge(P, m7, P.lab[b7], w, lab7, words);
+                if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], w, lab6, words);
+                if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], w, lab7, words);
                 inA += a; inR += r; inAR += a && r;
                 p = S.pid[i][p];
             }
@@ -720,8 +756,8 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
         }
         {   // the task's own vertex (never in a row it owns: same6/same7 exclude b6/b7)
             bool a = false, r = false;
-            if ((P.two_same6 >> l) & 1u) a = ((P.two_adj6 >> l) & 1u) || has_edge(P, m6, P.lab[b6], v, lab6, words);
-            if ((P.two_same7 >> l) & 1u) r = ((P.two_adj7 >> l) & 1u) || has_edge(P, m7, P.lab[b7], v, lab7, words);
+            if ((P.two_same6 >> l) & 1u) a = ((P.two_adj6 >> l) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], v, lab6, words);
+            if ((P.two_same7 >> l) & 1u) r = ((P.two_adj7 >> l) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], v, lab7, words);
             inA += a; inR += r; inAR += a && r;
         }
     }
@@ -741,6 +777,10 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
             S.tacc[lane] = 0;
             __syncwarp();
             uint32_t ci = 0, cj = 0;
+#if GM_TWO_STAGE
+            uint32_t *stage = &LASTW(P.two_stage_row, 0);   // kStageWords words after the pair-count rows
+            uint32_t stage_tag = ~0u;                       // aligned start of the staged list
+#endif
             while (true) {
                 // fast path: the cursor's list alone fills the round (long lists against a hub)
                 const uint32_t sl_ci = __shfl_sync(FULL, sl, ci & 31);
@@ -768,7 +808,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                         const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
                         uint32_t wv[4];
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) wv[g] = hit[g] ? hub_summ_word(P, f_gown, x[g], words) : 0u;
+                        for (int g = 0; g < 4; ++g) wv[g] = hit[g] ? hub_summ_word<(D > 8)>(P, f_gown, x[g], words) : 0u;
 #pragma unroll
                         for (int g = 0; g < 4; ++g) {
                             hit[g] = hit[g] && summ_says(wv[g], x[g]);
@@ -779,16 +819,35 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     } else {
                         // four lower bounds in the same list: the trip count is warp-uniform
                         uint32_t n = f_ge - f_gb, b[4] = {f_gb, f_gb, f_gb, f_gb};
+#if GM_TWO_STAGE
+                        const uint32_t *L = P.nbr;
+                        if (n && n <= kStageWords - 6) {   // the aligned superset fits the buffer
+                            const uint32_t a0 = f_gb & ~3u;
+                            if (a0 != stage_tag) {
+                                __syncwarp();
+                                if (lane == 0)
+                                    bulk_stage(stage, P.nbr + a0, 4u * (((f_ge + 3u) & ~3u) - a0), &S.mbar);
+                                mbar_wait(&S.mbar, stage_phase);
+                                stage_phase ^= 1u;
+                                stage_tag = a0;
+                            }
+                            L = stage - a0;                  // L[i] = nbr[i] for i in [a0, end)
+                        }
+#define GM_LD_L(i) (L[i])
+#else
+#define GM_LD_L(i) ld_nc(P.nbr + (i))
+#endif
                         while (n > 1) {
                             const uint32_t half = n >> 1;
 #pragma unroll
-                            for (int g = 0; g < 4; ++g) b[g] = (ld_nc(P.nbr + b[g] + half) <= x[g]) ? b[g] + half : b[g];
+                            for (int g = 0; g < 4; ++g) b[g] = (GM_LD_L(b[g] + half) <= x[g]) ? b[g] + half : b[g];
                             n -= half;
                             words += nval;
                         }
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) hit[g] = hit[g] && n == 1 && ld_nc(P.nbr + b[g]) == x[g];
+                        for (int g = 0; g < 4; ++g) hit[g] = hit[g] && n == 1 && GM_LD_L(b[g]) == x[g];
                         words += nval;
+#undef GM_LD_L
                     }
                     uint32_t h = 0;
 #pragma unroll
@@ -811,8 +870,8 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     bool hit, hit2 = false;
                     if (f_gown < P.nhubs) {
                         const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
-                        const uint32_t s1 = hub_summ_word(P, f_gown, x, words);
-                        const uint32_t s2 = step == 64 ? hub_summ_word(P, f_gown, x2, words) : 0u;
+                        const uint32_t s1 = hub_summ_word<(D > 8)>(P, f_gown, x, words);
+                        const uint32_t s2 = step == 64 ? hub_summ_word<(D > 8)>(P, f_gown, x2, words) : 0u;
                         const bool p1 = summ_says(s1, x), p2 = step == 64 && summ_says(s2, x2);
                         const uint32_t w1 = p1 ? ld_nc(row + (x >> 5)) : 0u;
                         const uint32_t w2 = p2 ? ld_nc(row + (x2 >> 5)) : 0u;
@@ -860,7 +919,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     ++words;
                     bool hit;
                     if (s_gown < P.nhubs) {
-                        hit = hub_bit(P, s_gown, x, words);
+                        hit = hub_bit<(D > 8)>(P, s_gown, x, words);
                     } else {
                         hit = contains(P.nbr, s_gb, s_ge, x, words);
                     }
@@ -900,12 +959,16 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
 
     unsigned long long my_count = 0, my_tasks = 0, my_rounds = 0, my_don = 0, my_words = 0;
     bool ovf = false;          // my_count wrapped (add_count)
+    uint32_t stage_phase = 0;  // GM_TWO_STAGE: parity of the staging mbarrier's next phase
+#if GM_TWO_STAGE
+    if (P.two_stage_row && lane == 0) mbar_init(&S.mbar);
+    __syncwarp();
+#endif
     uint32_t wacc = 0;
     uint32_t tick = 0;
     bool stop = false;
-    bool registered = false;   // this idle warp has posted a steal request
-    uint32_t home = P.team_rank;   // lineage rank of the unit this warp holds (gm_team)
-    uint32_t idle_polls = 0;       // failed polls since this warp went idle (team: remote requests)
+    // (the lineage rank of the unit this warp holds, gm_team, lives in S.home: read only on a
+    // donation and at the unit's end, it need not occupy a register through the search)
     // time limit relative to this launch: the first warp to start stamps t0
     if (P.limit_ns && lane == 0) atomicCAS(&C->t0, 0ull, globaltimer());
 
@@ -915,6 +978,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
         bool got = false;
         uint32_t backoff = 64;
         uint32_t src_rank = P.team_rank;     // ring the popped item came from
+        bool registered = false;             // this idle warp has posted a steal request
+        uint32_t idle_polls = 0;             // failed polls since then (team: remote requests)
         while (true) {
             unsigned long long b = ~0ull, item = ~0ull;
             int exit_now = 0;
@@ -958,7 +1023,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             exit_now = __shfl_sync(FULL, exit_now, 0);
             if (exit_now) { stop = true; break; }
             if (b != ~0ull) {
-                home = P.team_rank;             // a pool batch: this rank's lineage
+                if (lane == 0) S.home = P.team_rank;   // a pool batch: this rank's lineage
                 // pool batch: up to `batch` partial matches of depth d0 become the lanes of level d0-1
                 const unsigned long long k = min((unsigned long long)P.batch, P.pool_size - b);
                 const bool valid = lane < k;
@@ -991,7 +1056,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 S.cb[depth][lane] = lane == 0 ? it[1] : 0;
                 S.cl[depth][lane] = lane == 0 ? it[2] : 0;
                 S.cs[depth][lane] = (uint8_t)(lane == 0 ? it[3] : 0);
-                home = __shfl_sync(FULL, lane == 0 ? it[4] : 0u, 0);
+                if (lane == 0) S.home = it[4];
                 __syncwarp();
                 if (lane == 0) {   // release the slot for the next lap of the ring
                     if (P.team_n) {
@@ -1056,7 +1121,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         // reserve a ring slot
                         unsigned long long pos = ~0ull;
                         if (lane == 0) {
-                            work_add(P, C, home, 1);          // the new unit keeps this unit's lineage
+                            work_add(P, C, S.home, 1);        // the new unit keeps this unit's lineage
                             pos = VC->q_tail;
                             while (true) {
                                 // (slots are released by poppers, possibly on other GPUs)
@@ -1073,14 +1138,14 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                                     pos = VC->q_tail;
                                 }
                             }
-                            if (pos == ~0ull) work_add(P, C, home, -1);
+                            if (pos == ~0ull) work_add(P, C, S.home, -1);
                         }
                         pos = __shfl_sync(FULL, pos, 0);
                         if (pos == ~0ull) break;          // ring full: keep the work
                         if (lane == giver) {
                             uint32_t *it = P.q_items + (pos % P.q_cap) * kItemWords;
                             it[0] = (uint32_t)s; it[1] = S.cb[s][giver] + gb; it[2] = give; it[3] = S.cs[s][giver];
-                            it[4] = home; it[5] = P.epoch;
+                            it[4] = S.home; it[5] = P.epoch;
                             read_prefix<D>(S, s - 1, giver, it + 6);
                             S.cl[s][giver] = mask ? 0u : gb;
                             if (P.team_n) __threadfence_system(); else __threadfence();
@@ -1153,7 +1218,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             wacc = 0;
             if (!ENUM && P.bulk_two && l == last - 2) {
                 // pair counting: both remaining levels of every partial match at once
-                add_count(my_count, count_two<D>(P, S, scr, l, v, src, F, lane, wacc), ovf);
+                add_count(my_count, count_two<D>(P, S, scr, l, v, src, F, lane, wacc, stage_phase), ovf);
                 __syncwarp();
                 continue;
             }
@@ -1204,7 +1269,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             __syncwarp();
             ++l;
         }
-        if (lane == 0) work_add(P, C, home, -1);
+        if (lane == 0) work_add(P, C, S.home, -1);
     }
     // flush counters
     my_words += wacc;
@@ -1858,6 +1923,13 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             }
             uint32_t rl = P.bulk_last ? P.last_k + P.last_ka : 0u;
             if (P.bulk_two) rl = std::max<uint32_t>(rl, 6u);
+#if GM_TWO_STAGE
+            // staging buffer for the pair-count intersection (same-label leaves, two parents)
+            if (P.bulk_two && P.lab[p->nq - 2] == P.lab[p->nq - 1] && P.two_b6 != P.two_b7) {
+                P.two_stage_row = rl;
+                rl += kStageWords / 32;
+            }
+#endif
             P.rows_chk = rc;
             P.rows_last = rl;
         }
