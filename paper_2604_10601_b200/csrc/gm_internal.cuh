@@ -58,7 +58,8 @@ struct gm_graph {
     // two-level index for indexes larger than L2 (hubs.cu): bit b of hub h's summary row is 1
     // iff its bitmap has a set bit among vertices [256 b, 256 b + 256) (one 32-byte sector)
     uint32_t summ_words = 0;       // ceil(n / 8192) words per summary row; 0: no summary
-    uint32_t *hub_summ = nullptr;  // nhubs * summ_words
+    uint32_t summ_first = 0;       // hubs h >= summ_first have a summary row (selective enough)
+    uint32_t *hub_summ = nullptr;  // (nhubs - summ_first) * summ_words
 };
 
 namespace gm {

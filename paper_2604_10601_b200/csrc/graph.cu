@@ -247,7 +247,7 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
         rc = build_hubs(g, default_hub_budget(g), kDefaultHubMinDegree, -1, st);
         if (rc != GM_OK) goto cleanup;
         g->bytes = sizeof(uint32_t) * (rows + 1 + (nsel ? nsel : 1) + 3 * nn) +
-                   4ull * (uint64_t)g->nhubs * (g->hub_words + g->summ_words);
+                   4ull * ((uint64_t)g->nhubs * g->hub_words + (uint64_t)(g->nhubs - g->summ_first) * g->summ_words);
     }
 cleanup:
 #undef STEP
@@ -272,7 +272,7 @@ extern "C" int gm_graph_info(const gm_graph *g, gm_graph_info_t *info) {
     info->device_bytes = g->bytes;
     info->hubs = g->nhubs;
     info->hub_min_degree = g->hub_min_degree;
-    info->hub_bytes = 4ull * (uint64_t)g->nhubs * (g->hub_words + g->summ_words);
+    info->hub_bytes = 4ull * ((uint64_t)g->nhubs * g->hub_words + (uint64_t)(g->nhubs - g->summ_first) * g->summ_words);
     info->hub_summary_words = g->summ_words;
     info->reserved = 0;
     return GM_OK;

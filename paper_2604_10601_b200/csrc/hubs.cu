@@ -72,6 +72,7 @@ void free_hubs(gm_graph *g) {
     g->hub_bits = nullptr;
     g->hub_summ = nullptr;
     g->summ_words = 0;
+    g->summ_first = 0;
     g->nhubs = 0;
 }
 
@@ -103,12 +104,22 @@ int build_hubs(gm_graph *g, uint64_t budget_bytes, uint32_t min_degree, int summ
     int dev = 0, l2 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-    if (summary > 0 || (summary < 0 && per_hub * k > (uint64_t)l2)) {
+    // Only hubs whose summary is selective get one: a hub of degree d has neighbours in about
+    // 1 - exp(-256 d / n) of the blocks; above d = n / 1024 (~22 %) the extra dependent load
+    // costs more than the bitmap sectors it saves.  Hubs are in decreasing degree order, so
+    // the selective ones are a suffix [summ_first, k).
+    uint32_t first = 0;
+    if (summary < 1)
+        while (first < k && (uint64_t)(offs[first + 1] - offs[first]) * 1024 > g->n) ++first;
+    if (first < k && (summary > 0 || (summary < 0 && per_hub * k > (uint64_t)l2))) {
+        const uint32_t ks = k - first;
         g->summ_words = (uint32_t)((g->n + 8191) / 8192);
-        GM_CK(cudaMalloc(&g->hub_summ, 4ull * g->summ_words * k));
-        const uint64_t threads = (uint64_t)k * g->summ_words * 32;
+        g->summ_first = first;
+        GM_CK(cudaMalloc(&g->hub_summ, 4ull * g->summ_words * ks));
+        const uint64_t threads = (uint64_t)ks * g->summ_words * 32;
         const uint64_t blocks = std::min<uint64_t>((threads + 255) / 256, 148ull * 32);
-        k_hub_summ<<<(unsigned)blocks, 256, 0, st>>>(k, g->hub_words, g->summ_words, g->hub_bits, g->hub_summ);
+        k_hub_summ<<<(unsigned)blocks, 256, 0, st>>>(ks, g->hub_words, g->summ_words,
+                                                     g->hub_bits + (uint64_t)first * g->hub_words, g->hub_summ);
         GM_CK(cudaGetLastError());
     }
     GM_CK(cudaStreamSynchronize(st));

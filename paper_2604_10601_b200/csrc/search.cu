@@ -134,7 +134,7 @@ struct SearchParams {
     unsigned long long q_cap;
     const uint32_t *__restrict__ hub_bits;  // hub bitmaps (row w for device ids w < nhubs)
     const uint32_t *__restrict__ hub_summ;  // summary rows (1 bit per 256 vertices), or NULL
-    uint32_t summ_words;
+    uint32_t summ_words, summ_first;        // hubs h >= summ_first have row h - summ_first
     uint32_t nhubs;                         // 0: no hub index
     uint32_t hub_words;
     const uint32_t *__restrict__ new2old;   // device id -> original id (enumerate output)
@@ -223,9 +223,9 @@ __device__ __forceinline__ bool cand_bit(const SearchParams &P, uint32_t l, uint
 template <bool SUMM = true>
 __device__ __forceinline__ uint32_t hub_summ_word(const SearchParams &P, uint32_t h, uint32_t x, uint32_t &words) {
 #if GM_HUB_SUMMARY
-    if (SUMM && P.hub_summ) {
+    if (SUMM && P.hub_summ && h >= P.summ_first) {
         ++words;
-        return ld_nc(P.hub_summ + (unsigned long long)h * P.summ_words + (x >> 13));
+        return ld_nc(P.hub_summ + (unsigned long long)(h - P.summ_first) * P.summ_words + (x >> 13));
     }
 #endif
     return 0xffffffffu;
@@ -1657,6 +1657,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     P.hub_words = g->hub_words;
     P.hub_summ = g->hub_summ;
     P.summ_words = g->summ_words;
+    P.summ_first = g->summ_first;
     P.new2old = g->new2old;
     P.old2new = g->old2new;
     if (!W.ctrl) GM_CK(cudaMalloc(&W.ctrl, sizeof(Ctrl)));
