@@ -244,7 +244,8 @@ extern "C" int gm_load_graph(uint64_t n, uint64_t m, const uint32_t *src, const 
         STEP(cudaStreamSynchronize(st));
         cudaFree(k0); cudaFree(k1); cudaFree(tmp);   // release sort scratch before the hub index
         k0 = k1 = nullptr; tmp = nullptr;
-        rc = build_hubs(g, default_hub_budget(g), kDefaultHubMinDegree, -1, st);
+        // (no summary level by default: measured slower on rmat24/26)
+        rc = build_hubs(g, default_hub_budget(g), kDefaultHubMinDegree, 0, st);
         if (rc != GM_OK) goto cleanup;
         g->bytes = sizeof(uint32_t) * (rows + 1 + (nsel ? nsel : 1) + 3 * nn) +
                    4ull * ((uint64_t)g->nhubs * g->hub_words + (uint64_t)(g->nhubs - g->summ_first) * g->summ_words);

@@ -39,7 +39,7 @@ if os.environ.get("GM_HUB_MB"):                 # hub-index sweeps
     g.build_hubs(int(float(os.environ["GM_HUB_MB"]) * (1 << 20)), int(os.environ.get("GM_HUB_MIN", "64")),
                  int(os.environ.get("GM_HUB_SUMM", "-1")))
 q = qs[qi]
-p = gm.gm_plan_query(g, q)
+p = gm.gm_plan_query(g, q, filter=os.environ.get("GM_FILTER", "nlf"))
 u0 = p.info()["order"][0]
 cands = np.flatnonzero(p.candidates(u0))
 roots = np.random.default_rng(0).permutation(cands)[:nroots].astype(np.uint32) if nroots > 0 else None
