@@ -1,4 +1,5 @@
 set -x
+mkdir -p gpurun_out/r02
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 # filter / hub-budget experiments on rmat24 (every root, 1 s, tasks done)
 for q in 0 1 3; do
