@@ -70,6 +70,12 @@ constexpr uint32_t FULL = 0xffffffffu;
 #if GM_TWO_STAGE
 constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows per warp
 #endif
+#ifndef GM_WIDE
+#define GM_WIDE 1          // two tasks per lane per round at the terminal per-parent level
+#endif
+#ifndef GM_WIDE_MIN_D
+#define GM_WIDE_MIN_D 16   // ... in the kernels with at least this many stack levels
+#endif
 #ifndef GM_HUB_SUMMARY
 #define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
 #endif
@@ -536,6 +542,88 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         }
     }
     return ok;
+}
+
+// Process for TWO tasks per lane at a terminal per-parent level (wide rounds, GM_WIDE): the
+// same checks as process(..., par = true) -- filter bit, same-label injectivity against the
+// parent's list, one adjacency check per pass -- for tasks (v0, src0) and (v1, src1) in lock
+// step, so every lane keeps two independent probe chains in flight, both of them needed
+// (unlike a second check of one task, which is wasted when the first fails).
+template <int D>
+__device__ __forceinline__ void process_par2(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
+                                             uint32_t v0, uint32_t src0, bool has0, uint32_t v1, uint32_t src1,
+                                             bool has1, bool &F0, bool &F1, uint32_t &words) {
+    uint32_t cw0 = 0xffffffffu, cw1 = 0xffffffffu;
+    if ((P.cand_needed >> l) & 1u) {
+        if (has0) { cw0 = ld_nc(P.cand + P.candoff[l] + (v0 >> 5)); ++words; }
+        if (has1) { cw1 = ld_nc(P.cand + P.candoff[l] + (v1 >> 5)); ++words; }
+    }
+    bool ok0 = has0, ok1 = has1;
+    const uint32_t lab = P.lab[l];
+    const int nchk = __popc(P.bw[l]) - 1;
+    const int neq = __popc(P.same_lab[l] & ~P.bw[l]);
+    for (int e = 0; e < neq; ++e) {
+        ok0 = ok0 && (CHK(nchk + e, src0) != v0);
+        ok1 = ok1 && (CHK(nchk + e, src1) != v1);
+    }
+    ok0 = ok0 && ((cw0 >> (v0 & 31)) & 1u);
+    ok1 = ok1 && ((cw1 >> (v1 & 31)) & 1u);
+    for (int c = 0; c < nchk; ++c) {
+        if (!__any_sync(FULL, ok0 || ok1)) break;
+        const uint32_t w[2] = {CHK(c, src0), CHK(c, src1)};
+        const uint32_t vv[2] = {v0, v1};
+        const bool act[2] = {ok0, ok1};
+        uint32_t b[2] = {0, 0}, n[2] = {0, 0}, sw[2] = {0xffffffffu, 0xffffffffu}, hh[2] = {0, 0}, hx[2] = {0, 0};
+        bool r[2] = {true, true}, need[2] = {false, false}, hub[2] = {false, false};
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (!act[t]) continue;
+            if (w[t] < P.nhubs || (GM_VHUB && vv[t] < P.nhubs)) {
+                hh[t] = w[t] < P.nhubs ? w[t] : vv[t];
+                hx[t] = w[t] < P.nhubs ? vv[t] : w[t];
+                hub[t] = true;
+                sw[t] = hub_summ_word<(D > 8)>(P, hh[t], hx[t], words);
+            } else {
+                const uint32_t row = w[t] * P.S + lab;
+                b[t] = ld_nc(P.offs + row);
+                n[t] = ld_nc(P.offs + row + 1) - b[t];
+                need[t] = true;
+                words += 2;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (hub[t]) {
+                if (summ_says(sw[t], hx[t])) {
+                    ++words;
+                    r[t] = (ld_nc(P.hub_bits + (unsigned long long)hh[t] * P.hub_words + (hx[t] >> 5)) >> (hx[t] & 31)) & 1u;
+                } else {
+                    r[t] = false;
+                }
+            }
+        }
+        bool more = n[0] > 1 || n[1] > 1;
+        while (__any_sync(FULL, more)) {
+            more = false;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                if (n[t] > 1) {
+                    const uint32_t half = n[t] >> 1;
+                    b[t] = (ld_nc(P.nbr + b[t] + half) <= vv[t]) ? b[t] + half : b[t];
+                    n[t] -= half;
+                    ++words;
+                    more = more || n[t] > 1;
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+            if (need[t]) { r[t] = n[t] == 1 && ld_nc(P.nbr + b[t]) == vv[t]; words += n[t]; }
+        ok0 = ok0 && r[0];
+        ok1 = ok1 && r[1];
+    }
+    F0 = ok0;
+    F1 = ok1;
 }
 
 // The checks of the tasks at level l = P.par_level (the level holding almost all tasks: the
@@ -1159,6 +1247,76 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
             }
 
+#if GM_WIDE
+            // ---- wide round: at the terminal per-parent level (the set-counting level, else the
+            // last level; nothing descends from it) each lane takes TWO tasks of the virtual task
+            // pool, lane and lane + 32 (ScatterTask over 64 slots), and validates both in lock
+            // step (process_par2): twice the independent probes in flight per warp on the
+            // latency-bound DRAM-resident configs, with no probe wasted.
+            if (D >= GM_WIDE_MIN_D && !ENUM && !P.bulk_two && l == (int)P.par_level &&
+                (l == last || (P.bulk_last && l == last - 1))) {
+                const uint32_t ci = S.ci[l], cj = S.cj[l];
+                uint32_t src0, off0, src1, off1, k;
+                const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
+                if (ci < 32 && cl_ci - cj >= 64) {
+                    src0 = src1 = ci; off0 = cj + lane; off1 = cj + 32 + lane; k = 64;
+                    if (lane == 0) {
+                        if (cj + 64 < cl_ci) S.cj[l] = cj + 64;
+                        else { S.ci[l] = ci + 1; S.cj[l] = 0; }
+                    }
+                } else {
+                    uint32_t rem = 0;
+                    if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
+                    const uint32_t r64 = min(rem, 64u);
+                    uint32_t incl = r64;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t x = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= (uint32_t)o) incl += x;
+                    }
+                    const uint32_t total = __shfl_sync(FULL, incl, 31);
+                    if (total == 0) { --l; continue; }       // level exhausted: backtrack
+                    k = min(total, 64u);
+                    // source lane of task t = number of lanes whose inclusive count is <= t
+                    src0 = 0; src1 = 0;
+                    const uint32_t t1 = lane + 32;
+#pragma unroll
+                    for (uint32_t bb = 16; bb >= 1; bb >>= 1) {
+                        if (__shfl_sync(FULL, incl, src0 + bb - 1) <= lane) src0 += bb;
+                        if (__shfl_sync(FULL, incl, src1 + bb - 1) <= t1) src1 += bb;
+                    }
+                    src0 = min(src0, 31u); src1 = min(src1, 31u);
+                    const uint32_t ex0 = __shfl_sync(FULL, incl - r64, src0), ex1 = __shfl_sync(FULL, incl - r64, src1);
+                    off0 = lane < k ? lane - ex0 + (src0 == ci ? cj : 0) : 0;
+                    off1 = t1 < k ? t1 - ex1 + (src1 == ci ? cj : 0) : 0;
+                    // cursor after task k-1
+                    const uint32_t lt = (k - 1) & 31u;
+                    const uint32_t lsrc = k > 32 ? __shfl_sync(FULL, src1, lt) : __shfl_sync(FULL, src0, lt);
+                    const uint32_t loff = k > 32 ? __shfl_sync(FULL, off1, lt) : __shfl_sync(FULL, off0, lt);
+                    if (lane == 0) {
+                        if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
+                        else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
+                    }
+                }
+                const bool has0 = lane < k, has1 = lane + 32 < k;
+                const uint32_t v0 = has0 ? ld_nc(P.nbr + S.cb[l][src0] + off0) : 0;
+                const uint32_t v1 = has1 ? ld_nc(P.nbr + S.cb[l][src1] + off1) : 0;
+                my_rounds += (lane == 0) ? 2u : 0u;   // 64 task slots (idle rate: tasks / (32 rounds))
+                my_tasks += (uint32_t)has0 + (uint32_t)has1;
+                bool F0, F1;
+                process_par2<D>(P, S, scr, l, v0, src0, has0, v1, src1, has1, F0, F1, wacc);
+                my_words += wacc + (uint32_t)has0 + (uint32_t)has1;
+                wacc = 0;
+                if (l == last) {
+                    my_count += (uint32_t)F0 + (uint32_t)F1;
+                } else {
+                    if (F0) add_count(my_count, count_last<D>(P, S, scr, l, v0, src0, wacc), ovf);
+                    if (F1) add_count(my_count, count_last<D>(P, S, scr, l, v1, src1, wacc), ovf);
+                }
+                __syncwarp();
+                continue;
+            }
+#endif
             // ---- ScatterTask, warp-parallel: next 32 tasks of the virtual task pool at level l
             const uint32_t ci = S.ci[l], cj = S.cj[l];
             uint32_t src, off, k;
