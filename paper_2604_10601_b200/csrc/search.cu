@@ -74,7 +74,10 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #define GM_WIDE 1          // two tasks per lane per round at the terminal per-parent level
 #endif
 #ifndef GM_WIDE_MIN_D
-#define GM_WIDE_MIN_D 16   // ... in the kernels with at least this many stack levels
+#define GM_WIDE_MIN_D 8    // ... in the kernels with at least this many stack levels
+#endif
+#ifndef GM_WIDE_T
+#define GM_WIDE_T 2        // tasks per lane in a wide round
 #endif
 #ifndef GM_HUB_SUMMARY
 #define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
@@ -544,47 +547,55 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
     return ok;
 }
 
-// Process for TWO tasks per lane at a terminal per-parent level (wide rounds, GM_WIDE): the
+// Process for T tasks per lane at a terminal per-parent level (wide rounds, GM_WIDE): the
 // same checks as process(..., par = true) -- filter bit, same-label injectivity against the
-// parent's list, one adjacency check per pass -- for tasks (v0, src0) and (v1, src1) in lock
-// step, so every lane keeps two independent probe chains in flight, both of them needed
-// (unlike a second check of one task, which is wasted when the first fails).
-template <int D>
-__device__ __forceinline__ void process_par2(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
-                                             uint32_t v0, uint32_t src0, bool has0, uint32_t v1, uint32_t src1,
-                                             bool has1, bool &F0, bool &F1, uint32_t &words) {
-    uint32_t cw0 = 0xffffffffu, cw1 = 0xffffffffu;
-    if ((P.cand_needed >> l) & 1u) {
-        if (has0) { cw0 = ld_nc(P.cand + P.candoff[l] + (v0 >> 5)); ++words; }
-        if (has1) { cw1 = ld_nc(P.cand + P.candoff[l] + (v1 >> 5)); ++words; }
+// parent's list, one adjacency check per pass -- for tasks (v[t], src[t]) in lock step, so
+// every lane keeps T independent probe chains in flight, all of them needed (unlike a second
+// check of one task, which is wasted when the first fails).
+template <int D, int T>
+__device__ __forceinline__ void process_parT(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
+                                             const uint32_t (&v)[T], const uint32_t (&src)[T], const bool (&has)[T],
+                                             bool (&F)[T], uint32_t &words) {
+    uint32_t cw[T];
+    const bool filt = (P.cand_needed >> l) & 1u;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        cw[t] = 0xffffffffu;
+        if (filt && has[t]) { cw[t] = ld_nc(P.cand + P.candoff[l] + (v[t] >> 5)); ++words; }
     }
-    bool ok0 = has0, ok1 = has1;
+    bool ok[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) ok[t] = has[t];
     const uint32_t lab = P.lab[l];
     const int nchk = __popc(P.bw[l]) - 1;
     const int neq = __popc(P.same_lab[l] & ~P.bw[l]);
     for (int e = 0; e < neq; ++e) {
-        ok0 = ok0 && (CHK(nchk + e, src0) != v0);
-        ok1 = ok1 && (CHK(nchk + e, src1) != v1);
-    }
-    ok0 = ok0 && ((cw0 >> (v0 & 31)) & 1u);
-    ok1 = ok1 && ((cw1 >> (v1 & 31)) & 1u);
-    for (int c = 0; c < nchk; ++c) {
-        if (!__any_sync(FULL, ok0 || ok1)) break;
-        const uint32_t w[2] = {CHK(c, src0), CHK(c, src1)};
-        const uint32_t vv[2] = {v0, v1};
-        const bool act[2] = {ok0, ok1};
-        uint32_t b[2] = {0, 0}, n[2] = {0, 0}, sw[2] = {0xffffffffu, 0xffffffffu}, hh[2] = {0, 0}, hx[2] = {0, 0};
-        bool r[2] = {true, true}, need[2] = {false, false}, hub[2] = {false, false};
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            if (!act[t]) continue;
-            if (w[t] < P.nhubs || (GM_VHUB && vv[t] < P.nhubs)) {
-                hh[t] = w[t] < P.nhubs ? w[t] : vv[t];
-                hx[t] = w[t] < P.nhubs ? vv[t] : w[t];
+        for (int t = 0; t < T; ++t) ok[t] = ok[t] && (CHK(nchk + e, src[t]) != v[t]);
+    }
+    bool any = false;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        ok[t] = ok[t] && ((cw[t] >> (v[t] & 31)) & 1u);
+        any = any || ok[t];
+    }
+    for (int c = 0; c < nchk; ++c) {
+        if (!__any_sync(FULL, any)) break;
+        uint32_t b[T], n[T], sw[T], hh[T], hx[T];
+        bool r[T], need[T], hub[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            b[t] = 0; n[t] = 0; sw[t] = 0xffffffffu; hh[t] = 0; hx[t] = 0;
+            r[t] = true; need[t] = false; hub[t] = false;
+            if (!ok[t]) continue;
+            const uint32_t w = CHK(c, src[t]);
+            if (w < P.nhubs || (GM_VHUB && v[t] < P.nhubs)) {
+                hh[t] = w < P.nhubs ? w : v[t];
+                hx[t] = w < P.nhubs ? v[t] : w;
                 hub[t] = true;
                 sw[t] = hub_summ_word<(D > 8)>(P, hh[t], hx[t], words);
             } else {
-                const uint32_t row = w[t] * P.S + lab;
+                const uint32_t row = w * P.S + lab;
                 b[t] = ld_nc(P.offs + row);
                 n[t] = ld_nc(P.offs + row + 1) - b[t];
                 need[t] = true;
@@ -592,7 +603,7 @@ __device__ __forceinline__ void process_par2(const SearchParams &P, WarpStack<D>
             }
         }
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < T; ++t) {
             if (hub[t]) {
                 if (summ_says(sw[t], hx[t])) {
                     ++words;
@@ -602,28 +613,32 @@ __device__ __forceinline__ void process_par2(const SearchParams &P, WarpStack<D>
                 }
             }
         }
-        bool more = n[0] > 1 || n[1] > 1;
+        bool more = false;
+#pragma unroll
+        for (int t = 0; t < T; ++t) more = more || n[t] > 1;
         while (__any_sync(FULL, more)) {
             more = false;
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < T; ++t) {
                 if (n[t] > 1) {
                     const uint32_t half = n[t] >> 1;
-                    b[t] = (ld_nc(P.nbr + b[t] + half) <= vv[t]) ? b[t] + half : b[t];
+                    b[t] = (ld_nc(P.nbr + b[t] + half) <= v[t]) ? b[t] + half : b[t];
                     n[t] -= half;
                     ++words;
                     more = more || n[t] > 1;
                 }
             }
         }
+        any = false;
 #pragma unroll
-        for (int t = 0; t < 2; ++t)
-            if (need[t]) { r[t] = n[t] == 1 && ld_nc(P.nbr + b[t]) == vv[t]; words += n[t]; }
-        ok0 = ok0 && r[0];
-        ok1 = ok1 && r[1];
+        for (int t = 0; t < T; ++t) {
+            if (need[t]) { r[t] = n[t] == 1 && ld_nc(P.nbr + b[t]) == v[t]; words += n[t]; }
+            ok[t] = ok[t] && r[t];
+            any = any || ok[t];
+        }
     }
-    F0 = ok0;
-    F1 = ok1;
+#pragma unroll
+    for (int t = 0; t < T; ++t) F[t] = ok[t];
 }
 
 // The checks of the tasks at level l = P.par_level (the level holding almost all tasks: the
@@ -1249,26 +1264,29 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
 
 #if GM_WIDE
             // ---- wide round: at the terminal per-parent level (the set-counting level, else the
-            // last level; nothing descends from it) each lane takes TWO tasks of the virtual task
-            // pool, lane and lane + 32 (ScatterTask over 64 slots), and validates both in lock
-            // step (process_par2): twice the independent probes in flight per warp on the
-            // latency-bound DRAM-resident configs, with no probe wasted.
+            // last level; nothing descends from it) each lane takes WT tasks of the virtual task
+            // pool, lane + 32 j (ScatterTask over 32 WT slots), and validates them in lock step
+            // (process_parT): WT independent probe chains per lane, no probe wasted, and the
+            // per-round overheads (scatter, control checks, counting) paid once per 32 WT tasks.
             if (D >= GM_WIDE_MIN_D && !ENUM && !P.bulk_two && l == (int)P.par_level &&
                 (l == last || (P.bulk_last && l == last - 1))) {
+                constexpr int WT = GM_WIDE_T;
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
-                uint32_t src0, off0, src1, off1, k;
+                uint32_t tsrc[WT], toff[WT], k;
                 const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
-                if (ci < 32 && cl_ci - cj >= 64) {
-                    src0 = src1 = ci; off0 = cj + lane; off1 = cj + 32 + lane; k = 64;
+                if (ci < 32 && cl_ci - cj >= 32u * WT) {
+#pragma unroll
+                    for (int t = 0; t < WT; ++t) { tsrc[t] = ci; toff[t] = cj + 32u * t + lane; }
+                    k = 32u * WT;
                     if (lane == 0) {
-                        if (cj + 64 < cl_ci) S.cj[l] = cj + 64;
+                        if (cj + 32u * WT < cl_ci) S.cj[l] = cj + 32u * WT;
                         else { S.ci[l] = ci + 1; S.cj[l] = 0; }
                     }
                 } else {
                     uint32_t rem = 0;
                     if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
-                    const uint32_t r64 = min(rem, 64u);
-                    uint32_t incl = r64;
+                    const uint32_t rw = min(rem, 32u * WT);
+                    uint32_t incl = rw;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const uint32_t x = __shfl_up_sync(FULL, incl, o);
@@ -1276,42 +1294,56 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     }
                     const uint32_t total = __shfl_sync(FULL, incl, 31);
                     if (total == 0) { --l; continue; }       // level exhausted: backtrack
-                    k = min(total, 64u);
+                    k = min(total, 32u * WT);
                     // source lane of task t = number of lanes whose inclusive count is <= t
-                    src0 = 0; src1 = 0;
-                    const uint32_t t1 = lane + 32;
+#pragma unroll
+                    for (int t = 0; t < WT; ++t) tsrc[t] = 0;
 #pragma unroll
                     for (uint32_t bb = 16; bb >= 1; bb >>= 1) {
-                        if (__shfl_sync(FULL, incl, src0 + bb - 1) <= lane) src0 += bb;
-                        if (__shfl_sync(FULL, incl, src1 + bb - 1) <= t1) src1 += bb;
+#pragma unroll
+                        for (int t = 0; t < WT; ++t)
+                            if (__shfl_sync(FULL, incl, tsrc[t] + bb - 1) <= lane + 32u * t) tsrc[t] += bb;
                     }
-                    src0 = min(src0, 31u); src1 = min(src1, 31u);
-                    const uint32_t ex0 = __shfl_sync(FULL, incl - r64, src0), ex1 = __shfl_sync(FULL, incl - r64, src1);
-                    off0 = lane < k ? lane - ex0 + (src0 == ci ? cj : 0) : 0;
-                    off1 = t1 < k ? t1 - ex1 + (src1 == ci ? cj : 0) : 0;
-                    // cursor after task k-1
-                    const uint32_t lt = (k - 1) & 31u;
-                    const uint32_t lsrc = k > 32 ? __shfl_sync(FULL, src1, lt) : __shfl_sync(FULL, src0, lt);
-                    const uint32_t loff = k > 32 ? __shfl_sync(FULL, off1, lt) : __shfl_sync(FULL, off0, lt);
+#pragma unroll
+                    for (int t = 0; t < WT; ++t) {
+                        tsrc[t] = min(tsrc[t], 31u);
+                        const uint32_t ex = __shfl_sync(FULL, incl - rw, tsrc[t]);
+                        const uint32_t tt = lane + 32u * t;
+                        toff[t] = tt < k ? tt - ex + (tsrc[t] == ci ? cj : 0) : 0;
+                    }
+                    // cursor after task k-1 (held by lane (k-1) % 32 in slot (k-1) / 32)
+                    const uint32_t lt = (k - 1) & 31u, lj = (k - 1) >> 5;
+                    uint32_t ls = tsrc[0], lo = toff[0];
+#pragma unroll
+                    for (int t = 1; t < WT; ++t)
+                        if (lj == (uint32_t)t) { ls = tsrc[t]; lo = toff[t]; }
+                    const uint32_t lsrc = __shfl_sync(FULL, ls, lt), loff = __shfl_sync(FULL, lo, lt);
                     if (lane == 0) {
                         if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
                         else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
                     }
                 }
-                const bool has0 = lane < k, has1 = lane + 32 < k;
-                const uint32_t v0 = has0 ? ld_nc(P.nbr + S.cb[l][src0] + off0) : 0;
-                const uint32_t v1 = has1 ? ld_nc(P.nbr + S.cb[l][src1] + off1) : 0;
-                my_rounds += (lane == 0) ? 2u : 0u;   // 64 task slots (idle rate: tasks / (32 rounds))
-                my_tasks += (uint32_t)has0 + (uint32_t)has1;
-                bool F0, F1;
-                process_par2<D>(P, S, scr, l, v0, src0, has0, v1, src1, has1, F0, F1, wacc);
-                my_words += wacc + (uint32_t)has0 + (uint32_t)has1;
+                uint32_t tv[WT];
+                bool th[WT], tf[WT];
+                uint32_t nh = 0;
+#pragma unroll
+                for (int t = 0; t < WT; ++t) {
+                    th[t] = lane + 32u * t < k;
+                    tv[t] = th[t] ? ld_nc(P.nbr + S.cb[l][tsrc[t]] + toff[t]) : 0;
+                    nh += th[t];
+                }
+                my_rounds += (lane == 0) ? (uint32_t)WT : 0u;   // 32 WT task slots (idle rate)
+                my_tasks += nh;
+                process_parT<D, WT>(P, S, scr, l, tv, tsrc, th, tf, wacc);
+                my_words += wacc + nh;
                 wacc = 0;
                 if (l == last) {
-                    my_count += (uint32_t)F0 + (uint32_t)F1;
+#pragma unroll
+                    for (int t = 0; t < WT; ++t) my_count += tf[t];
                 } else {
-                    if (F0) add_count(my_count, count_last<D>(P, S, scr, l, v0, src0, wacc), ovf);
-                    if (F1) add_count(my_count, count_last<D>(P, S, scr, l, v1, src1, wacc), ovf);
+#pragma unroll
+                    for (int t = 0; t < WT; ++t)
+                        if (tf[t]) add_count(my_count, count_last<D>(P, S, scr, l, tv[t], tsrc[t], wacc), ovf);
                 }
                 __syncwarp();
                 continue;
