@@ -77,7 +77,13 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #define GM_WIDE_MIN_D 8    // ... in the kernels with at least this many stack levels
 #endif
 #ifndef GM_WIDE_T
-#define GM_WIDE_T 2        // tasks per lane in a wide round
+#define GM_WIDE_T 2        // tasks per lane in a wide round (4: 12-30 % slower on rmat18/24)
+#endif
+#ifndef GM_WIDE_PAIR
+#define GM_WIDE_PAIR 1     // wide rounds also at the pair-counting level (leaves of different labels)
+#endif
+#ifndef GM_WIDE_T32
+#define GM_WIDE_T32 4      // ... in the 32-level kernel (4 vs 2: rmat26 +4 to +23 % tasks/s)
 #endif
 #ifndef GM_HUB_SUMMARY
 #define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
@@ -1268,9 +1274,12 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             // pool, lane + 32 j (ScatterTask over 32 WT slots), and validates them in lock step
             // (process_parT): WT independent probe chains per lane, no probe wasted, and the
             // per-round overheads (scatter, control checks, counting) paid once per 32 WT tasks.
-            if (D >= GM_WIDE_MIN_D && !ENUM && !P.bulk_two && l == (int)P.par_level &&
-                (l == last || (P.bulk_last && l == last - 1))) {
-                constexpr int WT = GM_WIDE_T;
+            // (also the pair-counting level when the two leaves have different labels: count_two
+            // is then per task, without the warp-collective intersection)
+            if (D >= GM_WIDE_MIN_D && !ENUM && l == (int)P.par_level &&
+                (P.bulk_two ? (GM_WIDE_PAIR && l == last - 2 && P.lab[last - 1] != P.lab[last])
+                            : (l == last || (P.bulk_last && l == last - 1)))) {
+                constexpr int WT = D >= 32 ? GM_WIDE_T32 : GM_WIDE_T;
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
                 uint32_t tsrc[WT], toff[WT], k;
                 const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
@@ -1337,7 +1346,11 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 process_parT<D, WT>(P, S, scr, l, tv, tsrc, th, tf, wacc);
                 my_words += wacc + nh;
                 wacc = 0;
-                if (l == last) {
+                if (P.bulk_two) {
+#pragma unroll
+                    for (int t = 0; t < WT; ++t)
+                        add_count(my_count, count_two<D>(P, S, scr, l, tv[t], tsrc[t], tf[t], lane, wacc, stage_phase), ovf);
+                } else if (l == last) {
 #pragma unroll
                     for (int t = 0; t < WT; ++t) my_count += tf[t];
                 } else {
