@@ -1344,6 +1344,14 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 my_rounds += (lane == 0) ? (uint32_t)WT : 0u;   // 32 WT task slots (idle rate)
                 my_tasks += nh;
                 process_parT<D, WT>(P, S, scr, l, tv, tsrc, th, tf, wacc);
+#ifdef GM_LEVEL_STATS
+                {
+                    uint32_t np = 0;
+#pragma unroll
+                    for (int t = 0; t < WT; ++t) np += __popc(__ballot_sync(FULL, tf[t]));
+                    if (lane == 0) { atomicAdd(&g_level_tasks[l], (unsigned long long)k); atomicAdd(&g_level_pass[l], (unsigned long long)np); }
+                }
+#endif
                 my_words += wacc + nh;
                 wacc = 0;
                 if (P.bulk_two) {
