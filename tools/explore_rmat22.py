@@ -31,3 +31,20 @@ for name in names:
                           "timed_out": st["timed_out"], "tasks": st["tasks"], "words": st["words"],
                           "idle": round(idle, 4), "aut": st["automorphisms"], "pool": st["pool_size"],
                           "depth": st["pool_depth"], "order": p.info()["order"]}), flush=True)
+
+# GM_SAMPLE=f: also estimate each pattern's total from a uniform sample of a fraction f of its
+# root candidates (root-restricted counts run without symmetry breaking)
+frac = float(os.environ.get("GM_SAMPLE", "0"))
+if frac > 0:
+    import numpy as np
+    for name in names:
+        q = mk[name]()
+        p = gm.gm_plan_query(g, q)
+        u0 = p.info()["order"][0]
+        cands = np.flatnonzero(p.candidates(u0))
+        k = max(1, int(len(cands) * frac))
+        roots = np.random.default_rng(7).permutation(cands)[:k].astype(np.uint32)
+        c, st = gm.gm_count(p, roots=roots, time_limit_ms=60000.0)
+        print(json.dumps({"q": name, "sample_roots": k, "of": int(len(cands)), "count": c,
+                          "est_total": c * len(cands) / k, "ms": round(st["total_ms"], 2),
+                          "timed_out": st["timed_out"], "tasks": st["tasks"]}), flush=True)
