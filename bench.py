@@ -451,8 +451,9 @@ def main():
 
     clocks = ClockSampler(gpu)
     clocks.start()
-    step_ms, dfs_ms, dfs_launches, words, kernel_launches = [], [], 0, 0, 0
+    step_ms, dfs_ms, dfs_launches, kernel_launches = [], [], 0, 0
     total_emb, timeouts, tasks, rounds = 0, 0, 0, 0
+    tasks_q = [0] * len(qs)
     q_ms_all, q_ms_solved = [], []
     per_query = None
     for k in range(args.steps):
@@ -471,10 +472,10 @@ def main():
         step_ms.append(s0.elapsed_time(s1))
         exact = partition.count_totals(halves)       # exact uint64 sums (no int64 wrap)
         total_emb += sum(exact)
-        for st, e0, e1 in res:
+        for i, (st, e0, e1) in enumerate(res):
             dfs_ms.append(st["dfs_ms"])
             dfs_launches += st["dfs_launches"]
-            words += st["words"]
+            tasks_q[i] += st["tasks"]
             tasks += st["tasks"]
             rounds += st["rounds"]
             kernel_launches += st["kernel_launches"] + 1       # + the filter kernel of the plan
@@ -490,8 +491,19 @@ def main():
 
     # ---- max over ranks
     T_ms, T_dfs = rank_max([sum(step_ms), sum(dfs_ms)])
-    words_all, tasks_all, rounds_all, launches_all, timeouts_all = rank_sums(
-        [words, tasks, rounds, kernel_launches, timeouts])
+    tasks_all, rounds_all, launches_all, timeouts_all = rank_sums([tasks, rounds, kernel_launches, timeouts])
+    tasks_q_all = rank_sums(tasks_q)
+
+    # ---- algorithmic words per task (the roofline's per-unit figure): one flushed counting pass
+    # of the same workload with GM_FLAG_COUNT_WORDS (the timed searches run the kernel compiled
+    # without the per-probe counters, which cost 12-23 % throughput); algorithmic bytes of the
+    # timed launches = sum over queries of tasks done x 4 x words per task of that query
+    cal = one_pass(qs, dict(count_words=True))["per_query"]
+    wpt = [r["words"] / r["tasks"] if r["tasks"] else 0.0 for r in cal]
+    words_all = sum(t * w for t, w in zip(tasks_q_all, wpt))
+    for r, w in zip(per_query, wpt):
+        r.pop("words", None)
+        r["words_per_task"] = round(w, 3)
     emb_per_step = total_emb / args.steps
     value = total_emb / (T_ms / 1e3)
 
@@ -628,6 +640,10 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_dfs", "launch_ms_mean": dfs_launch_ms,
                      "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peak_kind,
+                     "unit_of_work": "task T_M(u, v) (one candidate validation, PAPER.md:374)",
+                     "bytes_per_task": {r["q"]: round(4 * w, 3) for r, w in zip(cal, wpt)},
+                     "bytes_method": "4 x words per task (a flushed GM_FLAG_COUNT_WORDS pass of the same queries "
+                                     "and limits) x tasks done in the timed launches",
                      "share_of_step": T_dfs / T_ms if T_ms else None, "ncu": ncu},
         "gpu_launches": int(launches_all),
         "tasks_per_s": tasks_all / (T_ms / 1e3),

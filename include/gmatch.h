@@ -183,6 +183,12 @@ GM_API void gm_free_plan(gm_plan *p);
 #define GM_FLAG_NO_POOL      16u /* diagnostic (tests): this rank claims no pool batches and gets
                                     work only by stealing (needs steal = 1; with a team, from
                                     other ranks' rings) */
+#define GM_FLAG_COUNT_WORDS  32u /* gm_count: also count the algorithmic 4-byte words the DFS reads
+                                    (gm_run_stats.words; DESIGN.md §6 defines the unit).  The
+                                    counters cost 12-23 % throughput, so without this flag the
+                                    search runs a kernel compiled without them and words = 0. */
+#define GM_FLAG_NO_SIBLING   64u /* gm_count: never take the last level's candidates from the
+                                    recorded siblings of phi[last-1] (GM_PATH_SIBLING) */
 #define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
                                     Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)|.
                                     Symmetry breaking is also skipped when `roots` is given. */
@@ -241,10 +247,11 @@ typedef struct {
     uint32_t grid, block;     /* DFS launch shape */
     uint64_t words;           /* 4-byte words the DFS kernel read from the CSR and the candidate
                                  bitmaps: candidate reads + row-offset pairs + binary-search
-                                 probes + bitmap words (algorithmic bytes = 4 * words) */
+                                 probes + bitmap words (algorithmic bytes = 4 * words); 0 unless
+                                 GM_FLAG_COUNT_WORDS was set */
     uint64_t automorphisms;   /* |Aut(Q)| the count was scaled by (1: no symmetry breaking) */
     uint32_t paths;           /* GM_PATH_* bits: the exact shortcuts this call's DFS used */
-    uint32_t stack_levels;    /* levels D of the k_dfs stack instantiation (8, 16 or 32); 0: no DFS */
+    uint32_t stack_levels;    /* levels D of the k_dfs stack instantiation (8, 16, 24 (count only) or 32); 0: no DFS */
 } gm_run_stats;
 
 /* gm_run_stats.paths */
@@ -252,6 +259,8 @@ typedef struct {
 #define GM_PATH_PAIR_COUNT  2u  /* last two levels pair-counted (count_two) */
 #define GM_PATH_PAR_CHECKS  4u  /* per-parent check lists at the hot level (prep_checks) */
 #define GM_PATH_SYMMETRY    8u  /* symmetry-breaking conditions enforced (count x |Aut(Q)|) */
+#define GM_PATH_SIBLING    16u  /* last level's candidates from the recorded valid siblings of
+                                   phi[last-1] (clique-like last levels) */
 
 /*
  * gm_count -- count all embeddings of the plan's Q in G (this rank's share).

@@ -94,9 +94,28 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_PROBES_WIDE
 #define GM_PROBES_WIDE 1   // checks per pass in the 16/32-level kernels (process()): on rmat24 1 beat
 #endif                     // 2 by 3-15 % and 4 lost 13-51 % tasks/s (wasted DRAM probes)
+#ifndef GM_WORDS
+#define GM_WORDS 1         // count algorithmic words (gm_run_stats.words); 0 compiles the counting out
+#endif
+#if GM_WORDS
+#define GM_ADD_WORDS(x) (WORDS ? (void)(my_words += (x)) : (void)0)
+#else
+#define GM_ADD_WORDS(x) ((void)0)
+#endif
+#ifndef GM_D24
+#define GM_D24 1           // a 24-level count kernel for 17-24-vertex queries
+#endif
+#ifndef GM_SIB
+#define GM_SIB 1           // sibling prefixes for clique-like last levels (sib_append)
+#endif
+#ifndef GM_CUT_MIN
+#define GM_CUT_MIN 0       // GenerateTask under symmetry-breaking bounds: the backward row with the
+#endif                     // fewest candidates INSIDE the bounds (else: the shortest row, then cut)
 constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
 constexpr uint32_t kItemWords = 6 + kMaxQ;     // [depth, cb, cl, cs, home, epoch, prefix[kMaxQ]]
 constexpr uint32_t kMaxTeam = 8;               // ranks of a stealing team (gm_team)
+constexpr uint8_t kSibCs = 0xff;               // WarpStack.cs of a slice in the sibling buffer
+constexpr uint32_t kSibCap = 256;              // sibling-prefix entries per parent lane
 
 // Global control block.  Every field that many warps poll or update lives on its own
 // 128-byte line so that the pollers of one do not serialise the atomics of another.
@@ -187,6 +206,12 @@ struct SearchParams {
     uint32_t *team_items[kMaxTeam];
     unsigned long long *team_seq[kMaxTeam];
     uint32_t no_pool;           // GM_FLAG_NO_POOL (diagnostic): take no pool batches, only steal
+    // sibling prefixes: candidates of phi[sib_level] taken from the valid
+    // candidates of phi[sib_level - 1] under the same parent that precede the task's own vertex
+    uint32_t *sib;              // per warp: 32 parent lanes x sib_cap recorded siblings, or NULL
+    uint32_t sib_level;         // 0: off
+    uint32_t sib_cap;           // siblings recorded per parent (later ones use the normal slice)
+    uint32_t sib_chk;           // positions phi[sib_level] must still be checked against: bw \ bw(sib_level-1)
     unsigned long long limit_ns;     // time limit of this launch (0 = none)
 };
 
@@ -390,6 +415,7 @@ struct alignas(16) WarpStack {
     uint32_t tacc[32];    // pair counting: per-lane |A n R| accumulators
     unsigned long long mbar;  // GM_TWO_STAGE: mbarrier of the warp's bulk-copy staging buffer
     uint32_t home;            // gm_team: lineage rank of the unit this warp holds
+    uint32_t sibn[32];        // sibling prefixes: siblings recorded so far per parent lane
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
 };
@@ -409,24 +435,53 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
         best = 0xffffffffu;
         uint32_t lb = 0, ub = 0xffffffffu;     // symmetry breaking: candidates in [lb, ub)
         uint32_t p = lane;
-        for (int i = l - 1; i >= lowest; --i) {
-            const uint32_t w = S.v[i][p];
-            if ((bw >> i) & 1u) {
-                const uint32_t row = w * P.S + lab;
-                const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
-                words += 2;
-                if (hi - lo < best) { best = hi - lo; cb = lo; cs = (uint32_t)i; }
+        if (GM_CUT_MIN && (gt | lt)) {
+            // The bounds cut every backward row to [lb, ub); the fewest candidates are in the
+            // row whose CUT is shortest, which on degree-ordered ids is often not the shortest
+            // row (a low-degree vertex's neighbours are mostly high-degree, i.e. small ids).
+            // First the bounds, then each row's cut by two binary searches.
+            for (int i = l - 1; i >= lowest; --i) {
+                const uint32_t w = S.v[i][p];
+                if ((gt >> i) & 1u) lb = max(lb, w + 1);
+                if ((lt >> i) & 1u) ub = min(ub, w);
+                p = S.pid[i][p];
             }
-            if ((gt >> i) & 1u) lb = max(lb, w + 1);
-            if ((lt >> i) & 1u) ub = min(ub, w);
-            p = S.pid[i][p];
-        }
-        if (gt | lt) {   // the slice is sorted: cut it to the ids the conditions allow
-            uint32_t a = 0, e = best;
-            if (lb > 0 && best) a = lower_bound_idx(P.nbr + cb, best, lb, words);
-            if (ub != 0xffffffffu && best) e = lower_bound_idx(P.nbr + cb, best, ub, words);
-            cb += a;
-            best = e > a ? e - a : 0;
+            p = lane;
+            for (int i = l - 1; i >= lowest; --i) {
+                if ((bw >> i) & 1u) {
+                    const uint32_t row = S.v[i][p] * P.S + lab;
+                    const uint32_t lo = ld_nc(P.offs + row), len = ld_nc(P.offs + row + 1) - lo;
+                    words += 2;
+                    if (lb < ub && len) {
+                        const uint32_t a = lb ? lower_bound_idx(P.nbr + lo, len, lb, words) : 0u;
+                        const uint32_t e = ub != 0xffffffffu ? a + lower_bound_idx(P.nbr + lo + a, len - a, ub, words) : len;
+                        if (e - a < best) { best = e - a; cb = lo + a; cs = (uint32_t)i; }
+                    } else {
+                        best = 0; cb = lo; cs = (uint32_t)i;
+                    }
+                }
+                p = S.pid[i][p];
+            }
+        } else {
+            for (int i = l - 1; i >= lowest; --i) {
+                const uint32_t w = S.v[i][p];
+                if ((bw >> i) & 1u) {
+                    const uint32_t row = w * P.S + lab;
+                    const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
+                    words += 2;
+                    if (hi - lo < best) { best = hi - lo; cb = lo; cs = (uint32_t)i; }
+                }
+                if ((gt >> i) & 1u) lb = max(lb, w + 1);
+                if ((lt >> i) & 1u) ub = min(ub, w);
+                p = S.pid[i][p];
+            }
+            if (gt | lt) {   // the slice is sorted: cut it to the ids the conditions allow
+                uint32_t a = 0, e = best;
+                if (lb > 0 && best) a = lower_bound_idx(P.nbr + cb, best, lb, words);
+                if (ub != 0xffffffffu && best) e = lower_bound_idx(P.nbr + cb, best, ub, words);
+                cb += a;
+                best = e > a ? e - a : 0;
+            }
         }
     }
     S.cb[l][lane] = cb;
@@ -497,8 +552,8 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         bool r[G], need[G], hub[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            const bool act = ok && c + g < nchk;
-            w[g] = act ? CHK(c + g, ccol) : 0u;
+            w[g] = (ok && c + g < nchk) ? CHK(c + g, ccol) : 0u;
+            const bool act = ok && c + g < nchk && w[g] != ~0u;   // (~0u: no check, sibling prefix)
             r[g] = true; need[g] = false; hub[g] = false; b[g] = 0; n[g] = 0; hh[g] = 0; hx[g] = 0;
             sw[g] = 0xffffffffu;
             if (act) {
@@ -595,6 +650,7 @@ __device__ __forceinline__ void process_parT(const SearchParams &P, WarpStack<D>
             r[t] = true; need[t] = false; hub[t] = false;
             if (!ok[t]) continue;
             const uint32_t w = CHK(c, src[t]);
+            if (w == ~0u) continue;                  // no check in this row (sibling prefix)
             if (w < P.nhubs || (GM_VHUB && v[t] < P.nhubs)) {
                 hh[t] = w < P.nhubs ? w : v[t];
                 hx[t] = w < P.nhubs ? v[t] : w;
@@ -656,7 +712,13 @@ template <int D>
 __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, bool valid,
                                             uint32_t lane) {
     if (!valid) return;
-    const uint32_t chkm = P.bw[l] & ~(1u << S.cs[l][lane]), eqm = P.same_lab[l] & ~P.bw[l];
+    // a sibling-prefix slice (sib_append) already satisfies every check of phi[l-1] -- adjacency
+    // to its backward images, injectivity against the same-label images below, its bounds --
+    // so only the positions in sib_chk remain; unused rows hold ~0u ("no check": no vertex has
+    // that id, process() skips it and injectivity never matches it)
+    const bool sibl = (uint32_t)l == P.sib_level && S.cs[l][lane] == kSibCs;
+    const uint32_t chkm = sibl ? P.sib_chk : P.bw[l] & ~(1u << S.cs[l][lane]);
+    const uint32_t eqm = sibl ? 0u : P.same_lab[l] & ~P.bw[l];
     const int nchk = __popc(P.bw[l]) - 1;
     int kc = 0, ke = 0;
     uint32_t p = lane;
@@ -666,16 +728,60 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
         if ((eqm >> i) & 1u) { CHK(nchk + ke, lane) = w; ++ke; }
         p = S.pid[i][p];
     }
+    if (P.sib_level) {
+        for (int k = kc; k < nchk; ++k) CHK(k, lane) = ~0u;
+        const int neq = __popc(P.same_lab[l] & ~P.bw[l]);
+        for (int e = ke; e < neq; ++e) CHK(nchk + e, lane) = ~0u;
+    }
 #if GM_CHK_ORDER
     // most selective check first: larger device id = lower degree = fewer neighbours, so more
     // tasks fail early and whole warps leave the probe loop sooner
-    for (int a = 1; a < nchk; ++a) {
+    for (int a = 1; a < kc; ++a) {
         const uint32_t x = CHK(a, lane);
         int b = a - 1;
         while (b >= 0 && CHK(b, lane) < x) { CHK(b + 1, lane) = CHK(b, lane); --b; }
         CHK(b + 1, lane) = x;
     }
 #endif
+}
+
+// Sibling prefixes (count mode).  When phi[s] (s = P.sib_level, the last
+// position) is adjacent to phi[s-1] and to every backward neighbour of phi[s-1], has its label,
+// a candidate filter no stricter, and symmetry-breaking bounds that include M[phi[s]] <
+// M[phi[s-1]] and every bound of phi[s-1], then every valid image of phi[s] is a valid image
+// of phi[s-1] under the same parent M[0..s-2] that is smaller than M[phi[s-1]].  Those
+// siblings were all validated before M[phi[s-1]] itself (a slice is dealt in ascending
+// order), so recording each parent's valid siblings in order gives, for the task v that
+// just passed at level s-1, a complete candidate slice: the recorded prefix before v.  Its
+// tasks need only the checks in P.sib_chk (adjacency to v and to the backward neighbours
+// phi[s-1] lacks), against the |N(M[u'])|-long slice of §4.1 with every check.
+// Called by all lanes after generate(s) at the descent from level s-1 (v, src: the task of
+// this lane at level s-1 and its parent lane; F: it passed); keeps generate's slice when that
+// is shorter or the parent's buffer is full.
+template <int D>
+__device__ __forceinline__ void sib_append(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
+                                           bool F, uint32_t lane, uint32_t sib_base) {
+    const uint32_t grp = __match_any_sync(FULL, F ? src : 32u + lane);   // passing lanes per parent
+    const uint32_t pos = (F ? S.sibn[src] : 0u) + __popc(grp & ((1u << lane) - 1));
+    __syncwarp();
+    if (F) {
+        if (pos < P.sib_cap) {
+            const uint32_t o = sib_base + src * P.sib_cap;
+            P.sib[o + pos] = v;
+            if (pos <= S.cl[l + 1][lane]) { S.cb[l + 1][lane] = o; S.cl[l + 1][lane] = pos; S.cs[l + 1][lane] = kSibCs; }
+        }
+        if ((grp >> lane) == 1u) S.sibn[src] = pos + 1;   // the group's highest lane
+    }
+    __syncwarp();
+}
+
+// Candidate `off` of the slice of (level l, parent lane src): the CSR, or (sibling prefixes)
+// the warp's sibling buffer -- written during this launch, so read with a coherent load
+template <int D>
+__device__ __forceinline__ uint32_t cand_at(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t src, uint32_t off) {
+    const uint32_t cb = S.cb[l][src];
+    if (P.sib_level == (uint32_t)l && S.cs[l][src] == kSibCs) return P.sib[cb + off];
+    return ld_nc(P.nbr + cb + off);
 }
 
 // Last-level set counting (count mode): when phi[last] has ONE
@@ -1055,7 +1161,11 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 
 // ------------------------------------------------------------------ DFS kernel
 
-template <int D, bool ENUM>
+// WORDS: count the algorithmic words read (gm_run_stats.words, GM_FLAG_COUNT_WORDS).  The
+// counters are per-probe register adds in the hot loops; with WORDS = false they are dead code
+// and the compiler removes them (measured 12-23 % more throughput), so the timed
+// searches run without them and the bench takes words per task from a separate counting pass.
+template <int D, bool ENUM, bool WORDS>
 __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t *wbase = smem_raw + (size_t)(threadIdx.x >> 5) * P.warp_stride;
@@ -1063,6 +1173,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
     uint32_t *__restrict__ scr = reinterpret_cast<uint32_t *>(wbase + sizeof(WarpStack<D>));
     const uint32_t lane = threadIdx.x & 31;
     const int last = (int)P.nq - 1;
+    // this warp's sibling buffer (32 parent lanes x sib_cap words)
+    const uint32_t sib_base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u * P.sib_cap;
     Ctrl *C = P.ctrl;
     volatile Ctrl *VC = C;
 
@@ -1143,6 +1255,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
+                if (d0 + 1 == (int)P.sib_level) S.sibn[lane] = 0;
                 if (d0 == (int)P.par_level) prep_checks<D>(P, S, scr, d0, valid, lane);
                 if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, scr, d0, valid, lane, wacc);
                 if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
@@ -1176,6 +1289,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                     }
                 }
+                if ((int)depth + 1 == (int)P.sib_level) S.sibn[lane] = 0;
                 if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, scr, depth, lane == 0, lane);
                 if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
@@ -1208,7 +1322,9 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     // shallowest level with splittable untouched work (the last level's tasks
                     // are single checks: never worth a hand-off)
                     int served = 0;
-                    const int top = min(l, last - 1);
+                    // (sibling prefixes: neither level sib-1, whose siblings a parent records in
+                    // order, nor level sib, whose slices live in this warp's buffer)
+                    const int top = min(l, P.sib_level ? (int)P.sib_level - 2 : last - 1);
                     for (int s = base; s <= top && !served; ++s) {
                         const uint32_t ci = S.ci[s], cj = S.cj[s];
                         if (ci >= 32) continue;
@@ -1279,7 +1395,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (D >= GM_WIDE_MIN_D && !ENUM && l == (int)P.par_level &&
                 (P.bulk_two ? (GM_WIDE_PAIR && l == last - 2 && P.lab[last - 1] != P.lab[last])
                             : (l == last || (P.bulk_last && l == last - 1)))) {
-                constexpr int WT = D >= 32 ? GM_WIDE_T32 : GM_WIDE_T;
+                constexpr int WT = D > 16 ? GM_WIDE_T32 : GM_WIDE_T;
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
                 uint32_t tsrc[WT], toff[WT], k;
                 const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
@@ -1338,7 +1454,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
 #pragma unroll
                 for (int t = 0; t < WT; ++t) {
                     th[t] = lane + 32u * t < k;
-                    tv[t] = th[t] ? ld_nc(P.nbr + S.cb[l][tsrc[t]] + toff[t]) : 0;
+                    tv[t] = th[t] ? cand_at<D>(P, S, l, tsrc[t], toff[t]) : 0;
                     nh += th[t];
                 }
                 my_rounds += (lane == 0) ? (uint32_t)WT : 0u;   // 32 WT task slots (idle rate)
@@ -1352,7 +1468,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     if (lane == 0) { atomicAdd(&g_level_tasks[l], (unsigned long long)k); atomicAdd(&g_level_pass[l], (unsigned long long)np); }
                 }
 #endif
-                my_words += wacc + nh;
+                GM_ADD_WORDS(wacc + nh);
                 wacc = 0;
                 if (P.bulk_two) {
 #pragma unroll
@@ -1412,7 +1528,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
             }
             const bool has = lane < k;
-            const uint32_t v = has ? ld_nc(P.nbr + S.cb[l][src] + off) : 0;
+            const uint32_t v = has ? cand_at<D>(P, S, l, src, off) : 0;
             my_rounds += (lane == 0);
             my_tasks += has;
 #ifdef GM_LEVEL_STATS
@@ -1425,7 +1541,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (lane == 0) atomicAdd(&g_level_pass[l], (unsigned long long)__popc(__ballot_sync(FULL, F)));
             else __ballot_sync(FULL, F);
 #endif
-            my_words += wacc + (has ? 1u : 0u);
+            GM_ADD_WORDS(wacc + (has ? 1u : 0u));
             wacc = 0;
             if (!ENUM && P.bulk_two && l == last - 2) {
                 // pair counting: both remaining levels of every partial match at once
@@ -1473,6 +1589,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (!fm) continue;
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
             generate<D>(P, S, l + 1, F, lane, wacc);
+            if (l + 2 == (int)P.sib_level) S.sibn[lane] = 0;        // new parents of level sib-1
+            if (l + 1 == (int)P.sib_level) sib_append<D>(P, S, l, v, src, F, lane, sib_base);
             if (l + 1 == (int)P.par_level) prep_checks<D>(P, S, scr, l + 1, F, lane);
             if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, scr, l + 1, F, lane, wacc);
             if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, scr, l + 1, F, lane, wacc);
@@ -1483,7 +1601,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
         if (lane == 0) work_add(P, C, S.home, -1);
     }
     // flush counters
-    my_words += wacc;
+    GM_ADD_WORDS(wacc);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         add_count(my_count, __shfl_xor_sync(FULL, my_count, o), ovf);
@@ -1674,10 +1792,12 @@ struct Workspace {
     size_t tmp_bytes = 0;
     uint32_t *item_off = nullptr;   // per-item child counts / offsets of a BFS level (u64)
     size_t item_off_bytes = 0;
+    uint32_t *sib = nullptr;        // sibling-prefix buffers (every warp a grid can hold)
+    size_t sib_bytes = 0;
     int sms = 148;
     ~Workspace() {
         cudaFree(ctrl); cudaFree(q_items); cudaFree(q_seq); cudaFree(buf[0]); cudaFree(buf[1]);
-        cudaFree(tmp); cudaFree(item_off);
+        cudaFree(tmp); cudaFree(item_off); cudaFree(sib);
     }
 };
 
@@ -1695,12 +1815,12 @@ static int ensure(uint32_t *&p, size_t &have, size_t need) {
 template <int D>
 static size_t stack_bytes() { return sizeof(WarpStack<D>); }
 
-template <int D, bool ENUM>
+template <int D, bool ENUM, bool WORDS>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
     P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last));
     const size_t smem = (size_t)P.warp_stride * wpb;
-    auto kern = k_dfs<D, ENUM>;
+    auto kern = k_dfs<D, ENUM, WORDS>;
     GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int fit = 0;
     GM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, (int)(wpb * 32), smem));
@@ -2123,6 +2243,43 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                 P.par_low = need ? (uint32_t)__builtin_ctz(need) : l;
             }
         }
+        {   // sibling prefixes (sib_append): phi[last] adjacent to phi[last-1] and to all of its
+            // backward neighbours, same label, a filter no stricter (LDF: query degree, NLF:
+            // neighbour counts per label, each >= phi[last-1]'s), bounds including M[phi[last]] <
+            // M[phi[last-1]] and all of phi[last-1]'s; level last-1 searched by the DFS
+            const uint32_t last = p->nq - 1;
+            if (!enumerate && GM_SIB && !(o.flags & GM_FLAG_NO_SIBLING) && use_sb && last >= 2 &&
+                P.par_level == last && d + 1 <= last) {
+                const uint32_t a = p->order[last - 1], b = p->order[last];
+                const uint32_t bwa = p->bw[last - 1], bwb = p->bw[last];
+                bool ok = (bwb & bwa) == bwa && ((bwb >> (last - 1)) & 1u) && p->qlab[a] == p->qlab[b] &&
+                          ((P.sb_lt[last] >> (last - 1)) & 1u) && !(P.sb_gt[last - 1] & ~P.sb_gt[last]) &&
+                          !(P.sb_lt[last - 1] & ~P.sb_lt[last]);
+                if (ok && p->filter >= GM_FILTER_LDF) ok = p->qdeg[a] <= p->qdeg[b];
+                if (ok && p->filter >= GM_FILTER_NLF) {
+                    for (uint32_t x = 0; x < p->nq && ok; ++x) {
+                        const uint32_t L = p->qlab[x];
+                        uint32_t ca = 0, cb2 = 0;
+                        for (uint32_t y = 0; y < p->nq; ++y) {
+                            if (p->qlab[y] != L) continue;
+                            ca += (p->qadj[a] >> y) & 1u;
+                            cb2 += (p->qadj[b] >> y) & 1u;
+                        }
+                        ok = ca <= cb2;
+                    }
+                }
+                if (ok) {
+                    // one buffer row set per warp a grid can hold (<= 16 blocks of kDfsMaxWarps per SM)
+                    const size_t need = sizeof(uint32_t) * (size_t)W.sms * 16 * kDfsMaxWarps * 32 * kSibCap;
+                    rc = ensure(W.sib, W.sib_bytes, need);
+                    if (rc) return rc;
+                    P.sib = W.sib;
+                    P.sib_level = last;
+                    P.sib_cap = kSibCap;
+                    P.sib_chk = bwb & ~bwa;
+                }
+            }
+        }
         {   // scratch rows: the most check images any task (or a par-level parent) holds, and the
             // set / pair counting words
             const uint32_t last = p->nq - 1;
@@ -2147,19 +2304,28 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         }
         rs.paths = (P.bulk_last ? GM_PATH_SET_COUNT : 0u) | (P.bulk_two ? GM_PATH_PAIR_COUNT : 0u) |
                    (P.par_level != ~0u && P.par_level >= d ? GM_PATH_PAR_CHECKS : 0u) |
-                   (use_sb ? GM_PATH_SYMMETRY : 0u);
-        rs.stack_levels = p->nq <= 8 ? 8u : (p->nq <= 16 ? 16u : 32u);
+                   (use_sb ? GM_PATH_SYMMETRY : 0u) | (P.sib_level ? GM_PATH_SIBLING : 0u);
+        // stack depth: the smallest instantiation that holds the query (17-24-vertex counts get
+        // a 24-level stack: 11.6 KB per warp instead of 15.5, so more warps stay resident)
+        rs.stack_levels = p->nq <= 8 ? 8u : (p->nq <= 16 ? 16u : ((!enumerate && GM_D24 && p->nq <= 24) ? 24u : 32u));
         GM_CK(cudaEventRecord(d0e, st));
         const uint32_t nq = p->nq;
-        if (nq <= 8)
-            rc = enumerate ? launch_dfs<8, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block)
-                           : launch_dfs<8, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block);
+        const bool cw = (o.flags & GM_FLAG_COUNT_WORDS) != 0;
+        const uint32_t sharers = o.shared_pool_ctr ? o.world : 1u;
+#define GM_LAUNCH(DD, EE, WW) launch_dfs<DD, EE, WW>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
+        if (enumerate)   // (enumerate never counts words: its cost is the output)
+            rc = nq <= 8 ? GM_LAUNCH(8, true, false) : (nq <= 16 ? GM_LAUNCH(16, true, false) : GM_LAUNCH(32, true, false));
+        else if (nq <= 8)
+            rc = cw ? GM_LAUNCH(8, false, true) : GM_LAUNCH(8, false, false);
         else if (nq <= 16)
-            rc = enumerate ? launch_dfs<16, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block)
-                           : launch_dfs<16, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block);
+            rc = cw ? GM_LAUNCH(16, false, true) : GM_LAUNCH(16, false, false);
+#if GM_D24
+        else if (nq <= 24)
+            rc = cw ? GM_LAUNCH(24, false, true) : GM_LAUNCH(24, false, false);
+#endif
         else
-            rc = enumerate ? launch_dfs<32, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block)
-                           : launch_dfs<32, false>(P, W.sms, o.warps_per_block, o.blocks_per_sm, o.shared_pool_ctr ? o.world : 1u, st, &rs.grid, &rs.block);
+            rc = cw ? GM_LAUNCH(32, false, true) : GM_LAUNCH(32, false, false);
+#undef GM_LAUNCH
         if (rc) return rc;
         ++launches;
         rs.dfs_launches = 1;

@@ -1,4 +1,4 @@
-"""GPU parity for 9-32-vertex queries: the D=16 and D=32 instantiations of k_dfs.
+"""GPU parity for 9-32-vertex queries: the D=16, D=24 (count) and D=32 instantiations of k_dfs.
 
 The bench's configs 4 and 5 run 16-, 24- and 32-vertex dense queries (BASELINE.json
 configs[3..4]; the paper evaluates 8-, 12- and 16-vertex random queries, PAPER.md:883,
@@ -61,7 +61,8 @@ def with_leaves(core, k_leaves, same, seed):
 
 
 # (core size, seed, leaves, same-label leaves); every case verified to finish in the oracle in
-# a few seconds (R-MAT 12, 16 labels).  Sizes 10..32 cover k_dfs<16> (9-16) and k_dfs<32> (17-32).
+# a few seconds (R-MAT 12, 16 labels).  Sizes 10..32 cover k_dfs<16> (9-16), k_dfs<24> (17-24, count) and k_dfs<32>
+# (25-32; 17-32 when enumerating).
 DENSE = [(10, 1), (10, 3), (12, 1), (12, 3), (16, 1), (16, 3), (24, 1), (24, 3), (32, 1), (32, 2), (32, 3)]
 LEAVES = [(k, s, nl, same) for k in (10, 14, 22, 30) for s in (1, 3, 4) for nl, same in ((1, False), (2, False), (2, True))
           if not (k == 14 and s == 4 and same)]
@@ -95,10 +96,10 @@ def check_all_paths(env, q, order=None, expect_paths=0):
             c, st = gm.gm_count(p, tau=tau, steal=steal)
             assert c == ref, (q.name, tau, steal, st)
             if st["dfs_launches"]:
-                assert st["stack_levels"] == (16 if q.n <= 16 else 32)
+                assert st["stack_levels"] == (16 if q.n <= 16 else (24 if q.n <= 24 else 32))
             seen |= st["paths"]
     for kw in (dict(set_count=False), dict(pair_count=False), dict(symmetry=False),
-               dict(set_count=False, symmetry=False)):
+               dict(set_count=False, symmetry=False), dict(count_words=True)):
         for tau in (1, 64):
             c, st = gm.gm_count(p, tau=tau, **kw)
             assert c == ref, (q.name, kw, tau, st)

@@ -159,6 +159,9 @@ def test_count_random_small(gm, seed):
     assert c == ref, (q.edges.tolist(), q.labels.tolist(), st)
     c2, _ = gm.gm_count(p, tau=tau, set_count=False)      # every last-level task validated
     assert c2 == ref
+    c3, st3 = gm.gm_count(p, tau=tau, count_words=True)   # the word-counting kernel instantiation
+    assert c3 == ref
+    assert st["words"] == 0 and (st3["words"] > 0 or st3["dfs_launches"] == 0)
 
 
 @pytest.mark.parametrize("seed", range(16))
@@ -720,3 +723,58 @@ def test_enumerate_stop_at_capacity(gm):
         assert len(got) == 1000 and got <= refset
     rows, total, st = gm.gm_enumerate(p, capacity=len(ref) + 10, stop_at_capacity=True)
     assert total == len(ref) and st["timed_out"] == 0
+
+
+# ------------------------------------------------------------------ sibling prefixes
+
+def _sib_queries():
+    """Clique-like last levels (GM_PATH_SIBLING applies) and near misses (it must not)."""
+    qs = [gi.clique(4), gi.clique(5), gi.clique(6)]
+    # K4 plus a pendant vertex on the clique: last level is still clique-like under phi
+    qs.append(gi.Query(5, [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3), (3, 4)], [0] * 5, "k4tail"))
+    # diamond (K4 minus an edge): two triangles sharing an edge
+    qs.append(gi.Query(4, [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)], [0] * 4, "diamond"))
+    # labelled K4: two labels (the last two share one label or not, depending on the order)
+    qs.append(gi.Query(4, [(i, j) for i in range(4) for j in range(i + 1, 4)], [0, 0, 1, 1], "k4lab"))
+    qs.append(gi.Query(5, [(i, j) for i in range(5) for j in range(i + 1, 5)], [0, 0, 0, 1, 1], "k5lab"))
+    return qs
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sibling_prefix_counts(gm, seed):
+    """Sibling prefixes: counts with and without them equal the oracle's, on
+    R-MAT and ER graphs with hubs whose sibling lists overflow the per-parent buffer, with
+    the pool starting below the sibling level (tau = 1) or not, stealing on and off."""
+    if seed % 2:
+        n, s, d = gi.er_edges(100, 36.0, seed)
+    else:
+        n, s, d = gi.rmat_edges(9, 8, seed)
+    nl = 1 if seed < 4 else 2
+    lab = gi.uniform_labels(n, nl, seed)
+    og = OracleGraph(n, s, d, lab)
+    g = gm.gm_load_graph(n, s, d, lab, nl)
+    seen = 0
+    for q in _sib_queries():
+        if nl == 1 and len(set(q.labels.tolist())) > 1:
+            continue
+        if q.name == "clique6" and nl == 1 and seed % 2 == 0:
+            continue                                  # (the oracle needs ~25 s for it there)
+        ref = og.count(q)
+        p = gm.gm_plan_query(g, q)
+        for kw in (dict(tau=1), dict(tau=1, steal=False), dict(tau=64), dict(tau=10 ** 6),
+                   dict(tau=1, sibling=False), dict(tau=1, count_words=True)):
+            c, st = gm.gm_count(p, **kw)
+            assert c == ref, (q.name, kw, st)
+            seen |= st["paths"]
+    assert seen & 16, "no query took the sibling-prefix path"
+
+
+def test_sibling_prefix_closed_forms(gm):
+    """K_k in K_n = n!/(n-k)! with sibling prefixes (every sibling list of K_60 is long)."""
+    for n, k in ((60, 4), (40, 5), (24, 6), (300, 4)):   # K_300: sibling lists overflow the buffer
+        nn, s, d = gi.complete_graph(n)
+        g = gm.gm_load_graph(nn, s, d)
+        p = gm.gm_plan_query(g, gi.clique(k))
+        c, st = gm.gm_count(p, tau=1)
+        assert c == math.factorial(n) // math.factorial(n - k)
+        assert st["paths"] & 16

@@ -25,5 +25,8 @@ for set in $SETS; do
     dense) run rmat18 100 0 0 1 2 3 > $OUT/ab_rmat18_dense.log 2>&1 ;;
     r24)   run rmat24 0 1000 0 1 2 3 > $OUT/ab_rmat24.log 2>&1 ;;
     r26)   run rmat26 0 1000 0 1 2 3 > $OUT/ab_rmat26.log 2>&1 ;;
+    r22)   for lib in "${LIBS[@]}"; do
+             GM_LIB=$lib timeout 300 python tools/explore_rmat22.py 5000 triangle clique4 cycle5 2>&1 | grep '^{' | sed "s|^|[${lib:-cur}] |"
+           done > $OUT/ab_rmat22.log 2>&1 ;;
   esac
 done

@@ -48,7 +48,8 @@ for it in range(2):
     c, st = gm.gm_count(p, roots=roots, tau=tau, time_limit_ms=float(os.environ.get("GM_LIMIT_MS", "0")),
                         warps_per_block=int(os.environ.get("GM_WPB", "0")),
                         blocks_per_sm=int(os.environ.get("GM_BPS", "0")),
-                        root_seed=int(os.environ.get("GM_ROOT_SEED", "0")))
+                        root_seed=int(os.environ.get("GM_ROOT_SEED", "0")),
+                        count_words=os.environ.get("GM_COUNT_WORDS", "0") == "1")
     print(q.name, len(q.edges), c, f"wall {time.time() - t:.3f}s",
           {k: st[k] for k in ("dfs_ms", "total_ms", "tasks", "words", "pool_size", "pool_depth", "donations",
                               "grid", "block")}, flush=True)
