@@ -79,6 +79,9 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_WIDE_T
 #define GM_WIDE_T 2        // tasks per lane in a wide round (4: 12-30 % slower on rmat18/24)
 #endif
+#ifndef GM_WIDE_T16
+#define GM_WIDE_T16 2      // ... in the 16-level kernel
+#endif
 #ifndef GM_WIDE_PAIR
 #define GM_WIDE_PAIR 1     // wide rounds also at the pair-counting level (leaves of different labels)
 #endif
@@ -498,7 +501,7 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
 // run in a uniform loop over the (uniform) number of backward neighbours, and the binary
 // searches step in lock-step until every lane is done (instead of per-lane early exits
 // that leave most of the warp idle; ncu measured 12 active lanes/warp before).
-template <int D>
+template <int D, bool SIB>
 __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, uint32_t v, uint32_t src,
                                         bool has, uint32_t lane, bool par, uint32_t &words) {
     // The candidate-bitmap word is loaded first and tested after the chain walk, so its L2
@@ -553,7 +556,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             w[g] = (ok && c + g < nchk) ? CHK(c + g, ccol) : 0u;
-            const bool act = ok && c + g < nchk && w[g] != ~0u;   // (~0u: no check, sibling prefix)
+            const bool act = ok && c + g < nchk && !(SIB && w[g] == ~0u);   // (~0u: no check, sibling prefix)
             r[g] = true; need[g] = false; hub[g] = false; b[g] = 0; n[g] = 0; hh[g] = 0; hx[g] = 0;
             sw[g] = 0xffffffffu;
             if (act) {
@@ -613,7 +616,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
 // parent's list, one adjacency check per pass -- for tasks (v[t], src[t]) in lock step, so
 // every lane keeps T independent probe chains in flight, all of them needed (unlike a second
 // check of one task, which is wasted when the first fails).
-template <int D, int T>
+template <int D, int T, bool SIB>
 __device__ __forceinline__ void process_parT(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
                                              const uint32_t (&v)[T], const uint32_t (&src)[T], const bool (&has)[T],
                                              bool (&F)[T], uint32_t &words) {
@@ -650,7 +653,7 @@ __device__ __forceinline__ void process_parT(const SearchParams &P, WarpStack<D>
             r[t] = true; need[t] = false; hub[t] = false;
             if (!ok[t]) continue;
             const uint32_t w = CHK(c, src[t]);
-            if (w == ~0u) continue;                  // no check in this row (sibling prefix)
+            if (SIB && w == ~0u) continue;           // no check in this row (sibling prefix)
             if (w < P.nhubs || (GM_VHUB && v[t] < P.nhubs)) {
                 hh[t] = w < P.nhubs ? w : v[t];
                 hx[t] = w < P.nhubs ? v[t] : w;
@@ -708,7 +711,7 @@ __device__ __forceinline__ void process_parT(const SearchParams &P, WarpStack<D>
 // entered, so that process() reads them by src instead of walking the pid chain per task:
 // the backward images other than the slice's source, then the same-label images that are
 // not backward neighbours (the only ones injectivity must compare: v in N(w) implies v != w).
-template <int D>
+template <int D, bool SIB>
 __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l, bool valid,
                                             uint32_t lane) {
     if (!valid) return;
@@ -716,7 +719,7 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
     // to its backward images, injectivity against the same-label images below, its bounds --
     // so only the positions in sib_chk remain; unused rows hold ~0u ("no check": no vertex has
     // that id, process() skips it and injectivity never matches it)
-    const bool sibl = (uint32_t)l == P.sib_level && S.cs[l][lane] == kSibCs;
+    const bool sibl = SIB && (uint32_t)l == P.sib_level && S.cs[l][lane] == kSibCs;
     const uint32_t chkm = sibl ? P.sib_chk : P.bw[l] & ~(1u << S.cs[l][lane]);
     const uint32_t eqm = sibl ? 0u : P.same_lab[l] & ~P.bw[l];
     const int nchk = __popc(P.bw[l]) - 1;
@@ -728,7 +731,7 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
         if ((eqm >> i) & 1u) { CHK(nchk + ke, lane) = w; ++ke; }
         p = S.pid[i][p];
     }
-    if (P.sib_level) {
+    if (SIB && P.sib_level) {
         for (int k = kc; k < nchk; ++k) CHK(k, lane) = ~0u;
         const int neq = __popc(P.same_lab[l] & ~P.bw[l]);
         for (int e = ke; e < neq; ++e) CHK(nchk + e, lane) = ~0u;
@@ -755,32 +758,30 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
 // just passed at level s-1, a complete candidate slice: the recorded prefix before v.  Its
 // tasks need only the checks in P.sib_chk (adjacency to v and to the backward neighbours
 // phi[s-1] lacks), against the |N(M[u'])|-long slice of §4.1 with every check.
-// Called by all lanes after generate(s) at the descent from level s-1 (v, src: the task of
-// this lane at level s-1 and its parent lane; F: it passed); keeps generate's slice when that
-// is shorter or the parent's buffer is full.
+// Called by all lanes at the descent from level s-1 (v, src: the task of this lane at level
+// s-1 and its parent lane; F: it passed): records v and returns its position in the parent's
+// list, i.e. the length of its prefix (a lane at position >= sib_cap keeps generate's slice:
+// the buffer holds only the first sib_cap siblings).
 template <int D>
-__device__ __forceinline__ void sib_append(const SearchParams &P, WarpStack<D> &S, int l, uint32_t v, uint32_t src,
-                                           bool F, uint32_t lane, uint32_t sib_base) {
+__device__ __forceinline__ uint32_t sib_append(const SearchParams &P, WarpStack<D> &S, uint32_t v, uint32_t src,
+                                               bool F, uint32_t lane, uint32_t sib_base) {
     const uint32_t grp = __match_any_sync(FULL, F ? src : 32u + lane);   // passing lanes per parent
     const uint32_t pos = (F ? S.sibn[src] : 0u) + __popc(grp & ((1u << lane) - 1));
     __syncwarp();
     if (F) {
-        if (pos < P.sib_cap) {
-            const uint32_t o = sib_base + src * P.sib_cap;
-            P.sib[o + pos] = v;
-            if (pos <= S.cl[l + 1][lane]) { S.cb[l + 1][lane] = o; S.cl[l + 1][lane] = pos; S.cs[l + 1][lane] = kSibCs; }
-        }
+        if (pos < P.sib_cap) P.sib[sib_base + src * P.sib_cap + pos] = v;
         if ((grp >> lane) == 1u) S.sibn[src] = pos + 1;   // the group's highest lane
     }
     __syncwarp();
+    return pos;
 }
 
 // Candidate `off` of the slice of (level l, parent lane src): the CSR, or (sibling prefixes)
 // the warp's sibling buffer -- written during this launch, so read with a coherent load
-template <int D>
+template <int D, bool SIB>
 __device__ __forceinline__ uint32_t cand_at(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t src, uint32_t off) {
     const uint32_t cb = S.cb[l][src];
-    if (P.sib_level == (uint32_t)l && S.cs[l][src] == kSibCs) return P.sib[cb + off];
+    if (SIB && P.sib_level == (uint32_t)l && S.cs[l][src] == kSibCs) return P.sib[cb + off];
     return ld_nc(P.nbr + cb + off);
 }
 
@@ -1165,7 +1166,9 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // counters are per-probe register adds in the hot loops; with WORDS = false they are dead code
 // and the compiler removes them (measured 12-23 % more throughput), so the timed
 // searches run without them and the bench takes words per task from a separate counting pass.
-template <int D, bool ENUM, bool WORDS>
+// SIB: the sibling-prefix code (sib_append) is compiled in; the instantiations without it
+// keep their register budget (the 8-level kernel spilled with it).
+template <int D, bool ENUM, bool WORDS, bool SIB>
 __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t *wbase = smem_raw + (size_t)(threadIdx.x >> 5) * P.warp_stride;
@@ -1174,7 +1177,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
     const uint32_t lane = threadIdx.x & 31;
     const int last = (int)P.nq - 1;
     // this warp's sibling buffer (32 parent lanes x sib_cap words)
-    const uint32_t sib_base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u * P.sib_cap;
+    const uint32_t sibL = SIB ? P.sib_level : 0u;
+    const uint32_t sib_base = SIB ? (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u * P.sib_cap : 0u;
     Ctrl *C = P.ctrl;
     volatile Ctrl *VC = C;
 
@@ -1255,8 +1259,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
-                if (d0 + 1 == (int)P.sib_level) S.sibn[lane] = 0;
-                if (d0 == (int)P.par_level) prep_checks<D>(P, S, scr, d0, valid, lane);
+                if (d0 + 1 == (int)sibL) S.sibn[lane] = 0;
+                if (d0 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, d0, valid, lane);
                 if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, scr, d0, valid, lane, wacc);
                 if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
                 base = d0; l = d0;
@@ -1289,8 +1293,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         ((volatile unsigned long long *)P.q_seq)[slot] = item + P.q_cap;
                     }
                 }
-                if ((int)depth + 1 == (int)P.sib_level) S.sibn[lane] = 0;
-                if ((int)depth == (int)P.par_level) prep_checks<D>(P, S, scr, depth, lane == 0, lane);
+                if ((int)depth + 1 == (int)sibL) S.sibn[lane] = 0;
+                if ((int)depth == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, depth, lane == 0, lane);
                 if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 base = (int)depth; l = (int)depth;
@@ -1324,7 +1328,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     int served = 0;
                     // (sibling prefixes: neither level sib-1, whose siblings a parent records in
                     // order, nor level sib, whose slices live in this warp's buffer)
-                    const int top = min(l, P.sib_level ? (int)P.sib_level - 2 : last - 1);
+                    const int top = min(l, sibL ? (int)sibL - 2 : last - 1);
                     for (int s = base; s <= top && !served; ++s) {
                         const uint32_t ci = S.ci[s], cj = S.cj[s];
                         if (ci >= 32) continue;
@@ -1395,7 +1399,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (D >= GM_WIDE_MIN_D && !ENUM && l == (int)P.par_level &&
                 (P.bulk_two ? (GM_WIDE_PAIR && l == last - 2 && P.lab[last - 1] != P.lab[last])
                             : (l == last || (P.bulk_last && l == last - 1)))) {
-                constexpr int WT = D > 16 ? GM_WIDE_T32 : GM_WIDE_T;
+                constexpr int WT = D > 16 ? GM_WIDE_T32 : (D > 8 ? GM_WIDE_T16 : GM_WIDE_T);
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
                 uint32_t tsrc[WT], toff[WT], k;
                 const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
@@ -1454,12 +1458,12 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
 #pragma unroll
                 for (int t = 0; t < WT; ++t) {
                     th[t] = lane + 32u * t < k;
-                    tv[t] = th[t] ? cand_at<D>(P, S, l, tsrc[t], toff[t]) : 0;
+                    tv[t] = th[t] ? cand_at<D, SIB>(P, S, l, tsrc[t], toff[t]) : 0;
                     nh += th[t];
                 }
                 my_rounds += (lane == 0) ? (uint32_t)WT : 0u;   // 32 WT task slots (idle rate)
                 my_tasks += nh;
-                process_parT<D, WT>(P, S, scr, l, tv, tsrc, th, tf, wacc);
+                process_parT<D, WT, SIB>(P, S, scr, l, tv, tsrc, th, tf, wacc);
 #ifdef GM_LEVEL_STATS
                 {
                     uint32_t np = 0;
@@ -1528,7 +1532,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
             }
             const bool has = lane < k;
-            const uint32_t v = has ? cand_at<D>(P, S, l, src, off) : 0;
+            const uint32_t v = has ? cand_at<D, SIB>(P, S, l, src, off) : 0;
             my_rounds += (lane == 0);
             my_tasks += has;
 #ifdef GM_LEVEL_STATS
@@ -1536,7 +1540,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
 #endif
 
             // ---- Process
-            const bool F = process<D>(P, S, scr, l, v, src, has, lane, l == (int)P.par_level, wacc);
+            const bool F = process<D, SIB>(P, S, scr, l, v, src, has, lane, l == (int)P.par_level, wacc);
 #ifdef GM_LEVEL_STATS
             if (lane == 0) atomicAdd(&g_level_pass[l], (unsigned long long)__popc(__ballot_sync(FULL, F)));
             else __ballot_sync(FULL, F);
@@ -1588,10 +1592,20 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             __syncwarp();
             if (!fm) continue;
             // ---- descend: GenerateTask for level l+1 on the lanes that extended
-            generate<D>(P, S, l + 1, F, lane, wacc);
-            if (l + 2 == (int)P.sib_level) S.sibn[lane] = 0;        // new parents of level sib-1
-            if (l + 1 == (int)P.sib_level) sib_append<D>(P, S, l, v, src, F, lane, sib_base);
-            if (l + 1 == (int)P.par_level) prep_checks<D>(P, S, scr, l + 1, F, lane);
+            if (SIB && l + 1 == (int)sibL) {
+                // sibling prefix when the buffer holds it (no GenerateTask), else the usual slice
+                const uint32_t pos = sib_append<D>(P, S, v, src, F, lane, sib_base);
+                const bool sibok = F && pos < P.sib_cap;
+                generate<D>(P, S, l + 1, F && !sibok, lane, wacc);
+                if (sibok) {
+                    S.cb[l + 1][lane] = sib_base + src * P.sib_cap; S.cl[l + 1][lane] = pos;
+                    S.cs[l + 1][lane] = kSibCs;
+                }
+            } else {
+                generate<D>(P, S, l + 1, F, lane, wacc);
+            }
+            if (SIB && l + 2 == (int)sibL) S.sibn[lane] = 0;        // new parents of level sib-1
+            if (l + 1 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, l + 1, F, lane);
             if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, scr, l + 1, F, lane, wacc);
             if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, scr, l + 1, F, lane, wacc);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
@@ -1815,12 +1829,12 @@ static int ensure(uint32_t *&p, size_t &have, size_t need) {
 template <int D>
 static size_t stack_bytes() { return sizeof(WarpStack<D>); }
 
-template <int D, bool ENUM, bool WORDS>
+template <int D, bool ENUM, bool WORDS, bool SIB = false>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
     P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last));
     const size_t smem = (size_t)P.warp_stride * wpb;
-    auto kern = k_dfs<D, ENUM, WORDS>;
+    auto kern = k_dfs<D, ENUM, WORDS, SIB>;
     GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int fit = 0;
     GM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, (int)(wpb * 32), smem));
@@ -2248,7 +2262,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             // neighbour counts per label, each >= phi[last-1]'s), bounds including M[phi[last]] <
             // M[phi[last-1]] and all of phi[last-1]'s; level last-1 searched by the DFS
             const uint32_t last = p->nq - 1;
-            if (!enumerate && GM_SIB && !(o.flags & GM_FLAG_NO_SIBLING) && use_sb && last >= 2 &&
+            if (!enumerate && GM_SIB && !(o.flags & GM_FLAG_NO_SIBLING) && use_sb && last >= 2 && p->nq <= 8 &&
                 P.par_level == last && d + 1 <= last) {
                 const uint32_t a = p->order[last - 1], b = p->order[last];
                 const uint32_t bwa = p->bw[last - 1], bwb = p->bw[last];
@@ -2315,6 +2329,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
 #define GM_LAUNCH(DD, EE, WW) launch_dfs<DD, EE, WW>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
         if (enumerate)   // (enumerate never counts words: its cost is the output)
             rc = nq <= 8 ? GM_LAUNCH(8, true, false) : (nq <= 16 ? GM_LAUNCH(16, true, false) : GM_LAUNCH(32, true, false));
+        else if (nq <= 8 && P.sib_level)   // (sibling prefixes: 8-level count kernels only)
+            rc = cw ? launch_dfs<8, false, true, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
+                    : launch_dfs<8, false, false, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block);
         else if (nq <= 8)
             rc = cw ? GM_LAUNCH(8, false, true) : GM_LAUNCH(8, false, false);
         else if (nq <= 16)
