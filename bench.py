@@ -46,7 +46,11 @@ CONFIGS = {
                  limit_ms=0.0, seed=11, desc="Erdos-Renyi G(n=1000, avg deg 8, 4 labels), tailed triangle"),
     "rmat22": dict(kind="rmat", scale=22, ef=16, labels=1, qsize=0, dense=[], sparse=[],
                    fixed=["triangle", "clique4", "cycle5"], limit_ms=5000.0, seed=3,
-                   desc="R-MAT scale 22 unlabelled (4.2M vertices, ~64M edges): triangle / 4-clique / 5-cycle"),
+                   desc="R-MAT scale 22 unlabelled (4.2M vertices, ~64M edges): triangle / 4-clique / 5-cycle",
+                   note="5-cycle: >= 3.9e14 embeddings (a uniform 0.2 % root sample, 3688 of 1.84M roots, found "
+                        "7.8e11 before its 60 s limit: profiles/r02/rmat22_sample.log), i.e. >= 3.9e13 "
+                        "symmetry-breaking representatives, each a validated last-level task: it cannot "
+                        "complete within the 5 s limit at any rate this path reaches (~7e9 per second)"),
     "rmat24": dict(kind="rmat", scale=24, ef=8, labels=16, qsize=16, dense=[1000, 1001, 1002, 1003],
                    sparse=[], limit_ms=2000.0, seed=4,
                    desc="LiveJournal-shaped R-MAT scale 24 (16.8M vertices, ~265M adjacency entries, 16 labels), "
@@ -619,6 +623,7 @@ def main():
         # per-GPU work (a time budget) is fixed as N grows
         "scaling": "weak" if limit > 0 else "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "queries": len(qs),
+                   **({"note": cfg["note"]} if cfg.get("note") else {}),
                    "per_query_time_limit_ms": limit,
                    "root_order": ("seeded pseudo-random root permutation (root_seed=1): a time-limited query "
                                   "counts the embeddings of a uniform sample of its roots"
