@@ -49,6 +49,9 @@ constexpr uint32_t FULL = 0xffffffffu;
 #ifndef GM_CHK_ORDER
 #define GM_CHK_ORDER 1
 #endif
+#ifndef GM_CHK_HUBFIRST
+#define GM_CHK_HUBFIRST 0
+#endif
 #ifndef GM_VHUB
 #define GM_VHUB 1
 #endif
@@ -82,6 +85,13 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_WIDE_T16
 #define GM_WIDE_T16 2      // ... in the 16-level kernel
 #endif
+#ifndef GM_WIDE_LOOP8
+#define GM_WIDE_LOOP8 0    // wide rounds' per-task counting in a loop (1) or unrolled (0): 8-level kernel
+#endif
+#ifndef GM_WIDE_LOOP16
+#define GM_WIDE_LOOP16 1   // ... 16/24/32-level kernels
+#endif
+#define GM_WIDE_LOOP_D(D) ((D) <= 8 ? GM_WIDE_LOOP8 : GM_WIDE_LOOP16)
 #ifndef GM_WIDE_PAIR
 #define GM_WIDE_PAIR 1     // wide rounds also at the pair-counting level (leaves of different labels)
 #endif
@@ -739,10 +749,13 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
 #if GM_CHK_ORDER
     // most selective check first: larger device id = lower degree = fewer neighbours, so more
     // tasks fail early and whole warps leave the probe loop sooner
+    // (GM_CHK_HUBFIRST, 16/32-level kernels: hubs first -- on DRAM-resident graphs a failing
+    // hub test costs one bitmap sector, a failing search the row offsets plus the search)
+    auto key = [&](uint32_t x) { return (GM_CHK_HUBFIRST && D > 8 && x < P.nhubs) ? (x | 0x80000000u) : x; };
     for (int a = 1; a < kc; ++a) {
-        const uint32_t x = CHK(a, lane);
+        const uint32_t x = CHK(a, lane), kx = key(x);
         int b = a - 1;
-        while (b >= 0 && CHK(b, lane) < x) { CHK(b + 1, lane) = CHK(b, lane); --b; }
+        while (b >= 0 && key(CHK(b, lane)) < kx) { CHK(b + 1, lane) = CHK(b, lane); --b; }
         CHK(b + 1, lane) = x;
     }
 #endif
@@ -940,8 +953,9 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
 // where |A n R| (b6 != b7) is one sorted-list intersection, computed by the whole warp
 // (shorter list split over the lanes, each element tested against the longer list's hub
 // bitmap or by binary search).  Warp-collective: every lane calls it; F = lane has a valid
-// partial match ending in (l, v, src).
-template <int D>
+// partial match ending in (l, v, src).  ISECT = false compiles the intersection out (callers
+// that only run it for leaves of different labels: the wide rounds).
+template <int D, bool ISECT = true>
 __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
                                                         uint32_t v, uint32_t src, bool F, uint32_t lane,
                                                         uint32_t &words, uint32_t &stage_phase) {
@@ -979,7 +993,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
     }
     const unsigned long long nV = (unsigned long long)(a1 - a0 - inA), nB = (unsigned long long)(r1 - r0 - inR);
     unsigned long long cnt = nV * nB;
-    if (lab6 == lab7) {                       // uniform
+    if (ISECT && lab6 == lab7) {              // uniform
         unsigned long long ar = 0;
         if (b6 == b7) {
             ar = a1 - a0;                     // A == R
@@ -1474,13 +1488,29 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
 #endif
                 GM_ADD_WORDS(wacc + nh);
                 wacc = 0;
-                if (P.bulk_two) {
-#pragma unroll
-                    for (int t = 0; t < WT; ++t)
-                        add_count(my_count, count_two<D>(P, S, scr, l, tv[t], tsrc[t], tf[t], lane, wacc, stage_phase), ovf);
-                } else if (l == last) {
+                if (l == last) {
 #pragma unroll
                     for (int t = 0; t < WT; ++t) my_count += tf[t];
+                } else if (GM_WIDE_LOOP_D(D)) {
+                    // one copy of count_two / count_last in a loop body instead of WT unrolled
+                    // copies (code size is an instruction-cache cost: ncu no_instruction stalls)
+#pragma unroll 1
+                    for (int t = 0; t < WT; ++t) {
+                        uint32_t vt = tv[0], st = tsrc[0];
+                        bool ft = tf[0];
+#pragma unroll
+                        for (int u = 1; u < WT; ++u)
+                            if (t == u) { vt = tv[u]; st = tsrc[u]; ft = tf[u]; }
+                        if (P.bulk_two)
+                            add_count(my_count, count_two<D, false>(P, S, scr, l, vt, st, ft, lane, wacc, stage_phase), ovf);
+                        else if (ft)
+                            add_count(my_count, count_last<D>(P, S, scr, l, vt, st, wacc), ovf);
+                    }
+                } else if (P.bulk_two) {
+                    // (different-label leaves only: count_two without its intersection)
+#pragma unroll
+                    for (int t = 0; t < WT; ++t)
+                        add_count(my_count, count_two<D, false>(P, S, scr, l, tv[t], tsrc[t], tf[t], lane, wacc, stage_phase), ovf);
                 } else {
 #pragma unroll
                     for (int t = 0; t < WT; ++t)

@@ -8,6 +8,7 @@ LIBS=()
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   if [ "$name" = cur ]; then LIBS+=(""); continue; fi
+  case $flags in *.so) LIBS+=("$flags"); continue ;; esac     # a prebuilt library
   tools/build_variant.sh /tmp/gm_$name.so paper_2604_10601_b200/csrc $flags && LIBS+=(/tmp/gm_$name.so)
 done
 run() {  # cfg nroots limit qi...
