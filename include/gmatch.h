@@ -189,6 +189,9 @@ GM_API void gm_free_plan(gm_plan *p);
                                     search runs a kernel compiled without them and words = 0. */
 #define GM_FLAG_NO_SIBLING   64u /* gm_count: never take the last level's candidates from the
                                     recorded siblings of phi[last-1] (GM_PATH_SIBLING) */
+#define GM_FLAG_NO_GEN_CACHE 128u /* gm_count/gm_enumerate: GenerateTask at the hot level computes
+                                    every backward row itself instead of reusing the part cached
+                                    per grandparent (diagnostic: results are identical) */
 #define GM_FLAG_NO_SYMMETRY  2u  /* gm_count: search every embedding instead of one per
                                     Aut(Q)-orbit (symmetry breaking, Appendix A) times |Aut(Q)|.
                                     Symmetry breaking is also skipped when `roots` is given. */

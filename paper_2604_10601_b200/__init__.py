@@ -181,7 +181,7 @@ def gm_plan_query(g: Graph, query, order=None, filter="nlf", stream=None) -> Pla
 def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=0, warps_per_block=0,
           time_limit_ms=0.0, roots=None, pool_bytes_max=0, set_count=True, symmetry=True, pair_count=True,
           shared_pool_ctr=None, root_seed=0, stop_at_capacity=False, team=None, no_pool=False,
-          count_words=False, sibling=True):
+          count_words=False, sibling=True, gen_cache=True):
     o = L.RunOpts()
     L.lib().gm_default_opts(ctypes.byref(o))
     if tau is not None:
@@ -217,6 +217,8 @@ def _opts(tau=None, rank=0, world=1, root_chunk=None, steal=True, blocks_per_sm=
         o.flags |= L.GM_FLAG_COUNT_WORDS
     if not sibling:
         o.flags |= L.GM_FLAG_NO_SIBLING
+    if not gen_cache:
+        o.flags |= L.GM_FLAG_NO_GEN_CACHE
     if team is not None:
         o.team = team._h
     if shared_pool_ctr is not None:

@@ -25,6 +25,7 @@ GM_FLAG_STOP_AT_CAPACITY = 8
 GM_FLAG_NO_POOL = 16
 GM_FLAG_COUNT_WORDS = 32
 GM_FLAG_NO_SIBLING = 64
+GM_FLAG_NO_GEN_CACHE = 128
 GM_TEAM_HANDLE_BYTES = 256
 GM_PATH_SET_COUNT, GM_PATH_PAIR_COUNT, GM_PATH_PAR_CHECKS, GM_PATH_SYMMETRY, GM_PATH_SIBLING = 1, 2, 4, 8, 16
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}

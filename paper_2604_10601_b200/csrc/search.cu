@@ -46,6 +46,7 @@ constexpr uint32_t FULL = 0xffffffffu;
 // then rows_last rows of set/pair-counting words
 #define CHK(k, x) scr[(k) * 32u + (x)]
 #define LASTW(k, x) scr[(P.rows_chk + (k)) * 32u + (x)]
+#define GENW(k, x) scr[(P.rows_chk + P.rows_last + (k)) * 32u + (x)]   // gen_prep's cached slice
 #ifndef GM_CHK_ORDER
 #define GM_CHK_ORDER 1
 #endif
@@ -120,6 +121,9 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #endif
 #ifndef GM_SIB
 #define GM_SIB 1           // sibling prefixes for clique-like last levels (sib_append)
+#endif
+#ifndef GM_GEN_CACHE
+#define GM_GEN_CACHE 1     // GenerateTask at the hot level with a per-grandparent cached part (gen_prep)
 #endif
 #ifndef GM_CUT_MIN
 #define GM_CUT_MIN 0       // GenerateTask under symmetry-breaking bounds: the backward row with the
@@ -203,6 +207,8 @@ struct SearchParams {
     uint32_t two_stage_row;     // GM_TWO_STAGE: first rows_last row of the staging buffer
     uint32_t rows_chk;          // scratch rows for check images (max checks of a task / par-level list)
     uint32_t rows_last;         // scratch rows for set/pair-counting words
+    uint32_t gen_level;         // GenerateTask of this level uses gen_prep's per-grandparent slice (0: off)
+    uint32_t rows_gen;          // scratch rows for it (5 or 0)
     uint32_t warp_stride;       // bytes of shared memory per warp: WarpStack + scratch rows
     uint32_t par_level;         // level whose checks are kept per parent (prep_checks), or ~0u
     uint32_t par_low;           // deepest level prep_checks visits
@@ -495,6 +501,89 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
                 cb += a;
                 best = e > a ? e - a : 0;
             }
+        }
+    }
+    S.cb[l][lane] = cb;
+    S.cl[l][lane] = best;
+    S.cs[l][lane] = (uint8_t)cs;
+}
+
+// GenerateTask with a per-grandparent part (GM_GEN_CACHE).  At level l = P.gen_level (the
+// level holding most tasks) every passing task of level l-1 calls GenerateTask, but the rows
+// of its backward neighbours mapped at levels <= l-2, and the symmetry bounds from those
+// levels, are the same for all children of one level-(l-2) partial match.  gen_prep computes
+// that part once per level-(l-2) lane when level l-1 is entered: the shortest such row, cut to
+// those bounds (GENW rows 0-2: begin, length, source level; rows 3-4: the bounds).  Then
+// generate_cached only looks at the row of level l-1 (when phi[l-1] is a backward neighbour)
+// and level l-1's bounds: the cached cut slice, cut further by them, or the level-(l-1) row
+// if its full length is shorter, cut by all bounds.  Any backward neighbour's row cut to the
+// bounds is a superset of the feasible set (§4.1), so either choice is exact.
+template <int D>
+__device__ __forceinline__ void gen_prep(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, bool valid,
+                                         uint32_t lane, uint32_t &words) {
+    if (!valid) return;
+    const int l = (int)P.gen_level;
+    const uint32_t below = (1u << (l - 1)) - 1;            // levels <= l-2
+    const uint32_t bw = P.bw[l] & below, gt = P.sb_gt[l] & below, lt = P.sb_lt[l] & below;
+    const uint32_t lab = P.lab[l];
+    uint32_t best = 0xffffffffu, cb = 0, cs = 0, lb = 0, ub = 0xffffffffu;
+    const int lowest = __ffs(bw | gt | lt) - 1;
+    uint32_t p = lane;
+    for (int i = l - 2; i >= lowest && lowest >= 0; --i) {
+        const uint32_t w = S.v[i][p];
+        if ((bw >> i) & 1u) {
+            const uint32_t row = w * P.S + lab;
+            const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
+            words += 2;
+            if (hi - lo < best) { best = hi - lo; cb = lo; cs = (uint32_t)i; }
+        }
+        if ((gt >> i) & 1u) lb = max(lb, w + 1);
+        if ((lt >> i) & 1u) ub = min(ub, w);
+        p = S.pid[i][p];
+    }
+    if (bw && (gt | lt)) {
+        uint32_t a = 0, e = best;
+        if (lb > 0 && best) a = lower_bound_idx(P.nbr + cb, best, lb, words);
+        if (ub != 0xffffffffu && best) e = lower_bound_idx(P.nbr + cb, best, ub, words);
+        cb += a;
+        best = e > a ? e - a : 0;
+    }
+    GENW(0, lane) = cb; GENW(1, lane) = best; GENW(2, lane) = cs; GENW(3, lane) = lb; GENW(4, lane) = ub;
+}
+
+template <int D>
+__device__ __forceinline__ void generate_cached(const SearchParams &P, WarpStack<D> &S, uint32_t *__restrict__ scr, int l,
+                                                bool valid, uint32_t lane, uint32_t &words) {
+    uint32_t best = 0, cb = 0, cs = 0;
+    if (valid) {
+        const uint32_t p = S.pid[l - 1][lane];
+        const uint32_t v1 = S.v[l - 1][lane];
+        const uint32_t nb = (P.bw[l] >> (l - 1)) & 1u;
+        const uint32_t ngt = (P.sb_gt[l] >> (l - 1)) & 1u, nlt = (P.sb_lt[l] >> (l - 1)) & 1u;
+        cb = GENW(0, p); best = GENW(1, p); cs = GENW(2, p);
+        uint32_t lo = 0, len = 0xffffffffu;
+        if (nb) {
+            const uint32_t row = v1 * P.S + P.lab[l];
+            lo = ld_nc(P.offs + row); len = ld_nc(P.offs + row + 1) - lo;
+            words += 2;
+        }
+        if (len < best) {
+            // the level-(l-1) row is shorter than the cached cut: cut it to every bound
+            const uint32_t lb = max(GENW(3, p), ngt ? v1 + 1 : 0u), ub = min(GENW(4, p), nlt ? v1 : 0xffffffffu);
+            uint32_t a = 0, e = len;
+            if (lb >= ub) { e = 0; }
+            else {
+                if (lb > 0 && len) a = lower_bound_idx(P.nbr + lo, len, lb, words);
+                if (ub != 0xffffffffu && len) e = lower_bound_idx(P.nbr + lo, len, ub, words);
+            }
+            cb = lo + a; best = e > a ? e - a : 0; cs = (uint32_t)(l - 1);
+        } else if (ngt | nlt) {
+            // the cached slice (already cut to the far bounds), cut to level l-1's bound
+            uint32_t a = 0, e = best;
+            if (ngt && best) a = lower_bound_idx(P.nbr + cb, best, v1 + 1, words);
+            if (nlt && best) e = lower_bound_idx(P.nbr + cb, best, v1, words);
+            cb += a;
+            best = e > a ? e - a : 0;
         }
     }
     S.cb[l][lane] = cb;
@@ -1274,6 +1363,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
                 if (d0 + 1 == (int)sibL) S.sibn[lane] = 0;
+                if (GM_GEN_CACHE && d0 + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, valid, lane, wacc);
                 if (d0 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, d0, valid, lane);
                 if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, scr, d0, valid, lane, wacc);
                 if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
@@ -1308,6 +1398,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     }
                 }
                 if ((int)depth + 1 == (int)sibL) S.sibn[lane] = 0;
+                if (GM_GEN_CACHE && (int)depth + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, lane == 0, lane, wacc);
                 if ((int)depth == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, depth, lane == 0, lane);
                 if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
@@ -1631,9 +1722,12 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     S.cb[l + 1][lane] = sib_base + src * P.sib_cap; S.cl[l + 1][lane] = pos;
                     S.cs[l + 1][lane] = kSibCs;
                 }
+            } else if (GM_GEN_CACHE && l + 1 == (int)P.gen_level) {
+                generate_cached<D>(P, S, scr, l + 1, F, lane, wacc);
             } else {
                 generate<D>(P, S, l + 1, F, lane, wacc);
             }
+            if (GM_GEN_CACHE && l + 2 == (int)P.gen_level) gen_prep<D>(P, S, scr, F, lane, wacc);
             if (SIB && l + 2 == (int)sibL) S.sibn[lane] = 0;        // new parents of level sib-1
             if (l + 1 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, l + 1, F, lane);
             if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, scr, l + 1, F, lane, wacc);
@@ -1862,7 +1956,7 @@ static size_t stack_bytes() { return sizeof(WarpStack<D>); }
 template <int D, bool ENUM, bool WORDS, bool SIB = false>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
-    P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last));
+    P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last + P.rows_gen));
     const size_t smem = (size_t)P.warp_stride * wpb;
     auto kern = k_dfs<D, ENUM, WORDS, SIB>;
     GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -2322,6 +2416,15 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                     P.sib_cap = kSibCap;
                     P.sib_chk = bwb & ~bwa;
                 }
+            }
+        }
+        {   // cached GenerateTask part at the hot level (gen_prep): when it has backward rows or
+            // bounds from levels <= l-2 and no sibling prefixes
+            const uint32_t l = P.par_level;
+            if (GM_GEN_CACHE && !(o.flags & GM_FLAG_NO_GEN_CACHE) && !P.sib_level && l != ~0u && l >= 2 &&
+                ((p->bw[l] | P.sb_gt[l] | P.sb_lt[l]) & ((1u << (l - 1)) - 1))) {
+                P.gen_level = l;
+                P.rows_gen = 5;
             }
         }
         {   // scratch rows: the most check images any task (or a par-level parent) holds, and the

@@ -99,7 +99,7 @@ def check_all_paths(env, q, order=None, expect_paths=0):
                 assert st["stack_levels"] == (16 if q.n <= 16 else (24 if q.n <= 24 else 32))
             seen |= st["paths"]
     for kw in (dict(set_count=False), dict(pair_count=False), dict(symmetry=False),
-               dict(set_count=False, symmetry=False), dict(count_words=True)):
+               dict(set_count=False, symmetry=False), dict(count_words=True), dict(gen_cache=False)):
         for tau in (1, 64):
             c, st = gm.gm_count(p, tau=tau, **kw)
             assert c == ref, (q.name, kw, tau, st)

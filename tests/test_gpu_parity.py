@@ -161,6 +161,8 @@ def test_count_random_small(gm, seed):
     assert c2 == ref
     c3, st3 = gm.gm_count(p, tau=tau, count_words=True)   # the word-counting kernel instantiation
     assert c3 == ref
+    c4, _ = gm.gm_count(p, tau=tau, gen_cache=False)       # GenerateTask without the cached part
+    assert c4 == ref
     assert st["words"] == 0 and (st3["words"] > 0 or st3["dfs_launches"] == 0)
 
 
@@ -762,7 +764,7 @@ def test_sibling_prefix_counts(gm, seed):
         ref = og.count(q)
         p = gm.gm_plan_query(g, q)
         for kw in (dict(tau=1), dict(tau=1, steal=False), dict(tau=64), dict(tau=10 ** 6),
-                   dict(tau=1, sibling=False), dict(tau=1, count_words=True)):
+                   dict(tau=1, sibling=False), dict(tau=1, count_words=True), dict(tau=1, sibling=False, gen_cache=False)):
             c, st = gm.gm_count(p, **kw)
             assert c == ref, (q.name, kw, st)
             seen |= st["paths"]
