@@ -262,6 +262,8 @@ typedef struct {
 #define GM_PATH_PAIR_COUNT  2u  /* last two levels pair-counted (count_two) */
 #define GM_PATH_PAR_CHECKS  4u  /* per-parent check lists at the hot level (prep_checks) */
 #define GM_PATH_SYMMETRY    8u  /* symmetry-breaking conditions enforced (count x |Aut(Q)|) */
+#define GM_PATH_GEN_CACHE  32u  /* GenerateTask at the hot level reused a part cached per
+                                   grandparent (gen_prep) */
 #define GM_PATH_SIBLING    16u  /* last level's candidates from the recorded valid siblings of
                                    phi[last-1] (clique-like last levels) */
 

@@ -28,6 +28,7 @@ GM_FLAG_NO_SIBLING = 64
 GM_FLAG_NO_GEN_CACHE = 128
 GM_TEAM_HANDLE_BYTES = 256
 GM_PATH_SET_COUNT, GM_PATH_PAIR_COUNT, GM_PATH_PAR_CHECKS, GM_PATH_SYMMETRY, GM_PATH_SIBLING = 1, 2, 4, 8, 16
+GM_PATH_GEN_CACHE = 32
 FILTERS = {"none": 0, "ldf": 1, "nlf": 2}
 
 # every symbol include/gmatch.h declares (checked by tests/test_abi.py)

@@ -83,6 +83,9 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_WIDE_T
 #define GM_WIDE_T 2        // tasks per lane in a wide round (4: 12-30 % slower on rmat18/24)
 #endif
+#ifndef GM_WIDE_TSIB
+#define GM_WIDE_TSIB 2     // ... in the 8-level sibling-prefix kernel (short prefix slices, one probe each)
+#endif
 #ifndef GM_WIDE_T16
 #define GM_WIDE_T16 2      // ... in the 16-level kernel
 #endif
@@ -1269,8 +1272,10 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // counters are per-probe register adds in the hot loops; with WORDS = false they are dead code
 // and the compiler removes them (measured 12-23 % more throughput), so the timed
 // searches run without them and the bench takes words per task from a separate counting pass.
-// SIB: the sibling-prefix code (sib_append) is compiled in; the instantiations without it
-// keep their register budget (the 8-level kernel spilled with it).
+// SIB: the code for symmetric unlabelled-style patterns is compiled in -- sibling prefixes
+// (sib_append) and the cached GenerateTask part (gen_prep); the instantiations without it keep
+// their register budget and code size (the 8-level kernel spilled with it, and the other
+// queries lost 10-30 % to the larger code).
 template <int D, bool ENUM, bool WORDS, bool SIB>
 __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1363,7 +1368,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
                 if (d0 + 1 == (int)sibL) S.sibn[lane] = 0;
-                if (GM_GEN_CACHE && d0 + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, valid, lane, wacc);
+                if (GM_GEN_CACHE && SIB && d0 + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, valid, lane, wacc);
                 if (d0 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, d0, valid, lane);
                 if (!ENUM && P.bulk_two && d0 == last - 2) prep_two<D>(P, S, scr, d0, valid, lane, wacc);
                 if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
@@ -1398,7 +1403,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     }
                 }
                 if ((int)depth + 1 == (int)sibL) S.sibn[lane] = 0;
-                if (GM_GEN_CACHE && (int)depth + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, lane == 0, lane, wacc);
+                if (GM_GEN_CACHE && SIB && (int)depth + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, lane == 0, lane, wacc);
                 if ((int)depth == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, depth, lane == 0, lane);
                 if (!ENUM && P.bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
@@ -1504,7 +1509,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (D >= GM_WIDE_MIN_D && !ENUM && l == (int)P.par_level &&
                 (P.bulk_two ? (GM_WIDE_PAIR && l == last - 2 && P.lab[last - 1] != P.lab[last])
                             : (l == last || (P.bulk_last && l == last - 1)))) {
-                constexpr int WT = D > 16 ? GM_WIDE_T32 : (D > 8 ? GM_WIDE_T16 : GM_WIDE_T);
+                constexpr int WT = D > 16 ? GM_WIDE_T32 : (D > 8 ? GM_WIDE_T16 : (SIB ? GM_WIDE_TSIB : GM_WIDE_T));
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
                 uint32_t tsrc[WT], toff[WT], k;
                 const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
@@ -1722,12 +1727,12 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     S.cb[l + 1][lane] = sib_base + src * P.sib_cap; S.cl[l + 1][lane] = pos;
                     S.cs[l + 1][lane] = kSibCs;
                 }
-            } else if (GM_GEN_CACHE && l + 1 == (int)P.gen_level) {
+            } else if (GM_GEN_CACHE && SIB && l + 1 == (int)P.gen_level) {
                 generate_cached<D>(P, S, scr, l + 1, F, lane, wacc);
             } else {
                 generate<D>(P, S, l + 1, F, lane, wacc);
             }
-            if (GM_GEN_CACHE && l + 2 == (int)P.gen_level) gen_prep<D>(P, S, scr, F, lane, wacc);
+            if (GM_GEN_CACHE && SIB && l + 2 == (int)P.gen_level) gen_prep<D>(P, S, scr, F, lane, wacc);
             if (SIB && l + 2 == (int)sibL) S.sibn[lane] = 0;        // new parents of level sib-1
             if (l + 1 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, l + 1, F, lane);
             if (!ENUM && P.bulk_two && l + 1 == last - 2) prep_two<D>(P, S, scr, l + 1, F, lane, wacc);
@@ -2420,9 +2425,13 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         }
         {   // cached GenerateTask part at the hot level (gen_prep): when it has backward rows or
             // bounds from levels <= l-2 and no sibling prefixes
+            // symmetry bounds (whose cut is the costly part: two binary searches per task) and a
+            // backward row, both from levels <= l-2; 8-level count kernels (measured: it helps
+            // the 5-cycle, +70 % embeddings in 5 s, and costs other queries)
             const uint32_t l = P.par_level;
-            if (GM_GEN_CACHE && !(o.flags & GM_FLAG_NO_GEN_CACHE) && !P.sib_level && l != ~0u && l >= 2 &&
-                ((p->bw[l] | P.sb_gt[l] | P.sb_lt[l]) & ((1u << (l - 1)) - 1))) {
+            const uint32_t far = l != ~0u && l >= 2 ? (1u << (l - 1)) - 1 : 0u;
+            if (GM_GEN_CACHE && !(o.flags & GM_FLAG_NO_GEN_CACHE) && !enumerate && p->nq <= 8 && !P.sib_level &&
+                far && (p->bw[l] & far) && ((P.sb_gt[l] | P.sb_lt[l]) & far)) {
                 P.gen_level = l;
                 P.rows_gen = 5;
             }
@@ -2451,7 +2460,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         }
         rs.paths = (P.bulk_last ? GM_PATH_SET_COUNT : 0u) | (P.bulk_two ? GM_PATH_PAIR_COUNT : 0u) |
                    (P.par_level != ~0u && P.par_level >= d ? GM_PATH_PAR_CHECKS : 0u) |
-                   (use_sb ? GM_PATH_SYMMETRY : 0u) | (P.sib_level ? GM_PATH_SIBLING : 0u);
+                   (use_sb ? GM_PATH_SYMMETRY : 0u) | (P.sib_level ? GM_PATH_SIBLING : 0u) |
+                   (P.gen_level ? GM_PATH_GEN_CACHE : 0u);
         // stack depth: the smallest instantiation that holds the query (17-24-vertex counts get
         // a 24-level stack: 11.6 KB per warp instead of 15.5, so more warps stay resident)
         rs.stack_levels = p->nq <= 8 ? 8u : (p->nq <= 16 ? 16u : ((!enumerate && GM_D24 && p->nq <= 24) ? 24u : 32u));
@@ -2462,7 +2472,7 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
 #define GM_LAUNCH(DD, EE, WW) launch_dfs<DD, EE, WW>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
         if (enumerate)   // (enumerate never counts words: its cost is the output)
             rc = nq <= 8 ? GM_LAUNCH(8, true, false) : (nq <= 16 ? GM_LAUNCH(16, true, false) : GM_LAUNCH(32, true, false));
-        else if (nq <= 8 && P.sib_level)   // (sibling prefixes: 8-level count kernels only)
+        else if (nq <= 8 && (P.sib_level || P.gen_level))   // (8-level count kernels only)
             rc = cw ? launch_dfs<8, false, true, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
                     : launch_dfs<8, false, false, true>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block);
         else if (nq <= 8)

@@ -780,3 +780,26 @@ def test_sibling_prefix_closed_forms(gm):
         c, st = gm.gm_count(p, tau=1)
         assert c == math.factorial(n) // math.factorial(n - k)
         assert st["paths"] & 16
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_generate_cache_counts(gm, seed):
+    """Cached GenerateTask part (gen_prep): symmetric unlabelled patterns whose
+    hot level has a backward row and symmetry bounds from levels <= l-2 (cycles, a house, a
+    bowtie), with and without the cache, against the oracle."""
+    n, s, d = gi.rmat_edges(7, 6, seed) if seed % 2 == 0 else gi.er_edges(60, 6.0, seed)
+    og = OracleGraph(n, s, d)
+    g = gm.gm_load_graph(n, s, d)
+    qs = [gi.cycle(5), gi.cycle(6)] + ([gi.cycle(7)] if seed % 2 else []) + [
+          gi.Query(5, [(0, 1), (1, 2), (2, 3), (3, 0), (2, 4), (3, 4)], [0] * 5, "house"),
+          gi.Query(5, [(0, 1), (1, 2), (0, 2), (2, 3), (3, 4), (2, 4)], [0] * 5, "bowtie")]
+    seen = 0
+    for q in qs:
+        ref = og.count(q)
+        p = gm.gm_plan_query(g, q)
+        for kw in (dict(tau=1), dict(tau=1, steal=False), dict(tau=64), dict(tau=1, gen_cache=False),
+                   dict(tau=1, count_words=True)):
+            c, st = gm.gm_count(p, **kw)
+            assert c == ref, (q.name, kw, st)
+            seen |= st["paths"]
+    assert seen & 32, "no query took the cached GenerateTask path"

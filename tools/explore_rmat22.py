@@ -25,7 +25,8 @@ for name in names:
     p = gm.gm_plan_query(g, q)
     for it in range(2):
         c, st = gm.gm_count(p, time_limit_ms=lim, root_seed=int(os.environ.get("GM_ROOT_SEED", "1")),
-                            symmetry=os.environ.get("GM_NOSYM") is None)
+                            symmetry=os.environ.get("GM_NOSYM") is None,
+                            gen_cache=os.environ.get("GM_GEN_CACHE", "1") == "1")
         idle = 1 - st["tasks"] / max(1, 32 * st["rounds"])
         print(json.dumps({"q": name, "count": c, "ms": round(st["total_ms"], 2), "dfs_ms": round(st["dfs_ms"], 2),
                           "timed_out": st["timed_out"], "tasks": st["tasks"], "words": st["words"],

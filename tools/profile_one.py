@@ -49,7 +49,8 @@ for it in range(2):
                         warps_per_block=int(os.environ.get("GM_WPB", "0")),
                         blocks_per_sm=int(os.environ.get("GM_BPS", "0")),
                         root_seed=int(os.environ.get("GM_ROOT_SEED", "0")),
-                        count_words=os.environ.get("GM_COUNT_WORDS", "0") == "1")
+                        count_words=os.environ.get("GM_COUNT_WORDS", "0") == "1",
+                        gen_cache=os.environ.get("GM_GEN_CACHE", "1") == "1")
     print(q.name, len(q.edges), c, f"wall {time.time() - t:.3f}s",
           {k: st[k] for k in ("dfs_ms", "total_ms", "tasks", "words", "pool_size", "pool_depth", "donations",
                               "grid", "block")}, flush=True)
