@@ -9,6 +9,9 @@ for c in rmat22 rmat24 rmat26; do
   timeout 900 python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-context > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 900 python bench.py --config rmat24 --steps 2 --warmup 3 --no-cpu-baseline --no-context --root-order hubs > $O/bench_rmat24_hubs.json 2> $O/bench_rmat24_hubs.err
+# the multi-rank path end to end: 2 ranks time-slicing one GPU (gloo for the host collectives)
+GM_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 2 --steps 1 --warmup 3 --no-context --no-cpu-baseline > $O/bench_2rank.json 2> $O/bench_2rank.err
 # launch list of a short bench run (the same command, fewer steps; under ncu every launch is serialised)
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_rmat18.csv \
   python bench.py --steps 1 --warmup 3 --no-context --no-cpu-baseline > $O/launches_bench.log 2>&1
