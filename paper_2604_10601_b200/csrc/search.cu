@@ -134,6 +134,7 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
 constexpr uint32_t kItemWords = 6 + kMaxQ;     // [depth, cb, cl, cs, home, epoch, prefix[kMaxQ]]
 constexpr uint32_t kMaxTeam = 8;               // ranks of a stealing team (gm_team)
+constexpr int kModePlain = 0, kModeSet = 1, kModePair = 2, kModePat = 3;   // k_dfs MODE
 constexpr uint8_t kSibCs = 0xff;               // WarpStack.cs of a slice in the sibling buffer
 constexpr uint32_t kSibCap = 256;              // sibling-prefix entries per parent lane
 
@@ -1276,11 +1277,15 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // (sib_append) and the cached GenerateTask part (gen_prep); the instantiations without it keep
 // their register budget and code size (the 8-level kernel spilled with it, and the other
 // queries lost 10-30 % to the larger code).
-// PAIR: the pair-counting code (count_two, prep_two) is compiled in; the kernels without it
-// (every query whose last two levels are not counted in bulk) are smaller, measured 14-18 %
-// faster on the rmat18 dense queries (instruction cache).
-template <int D, bool ENUM, bool WORDS, bool SIB, bool PAIR>
+// MODE: which counting code is compiled in -- kModePlain (none: every level by tasks),
+// kModeSet (last-level set counting), kModePair (set + pair counting), kModePat (set counting +
+// the pattern code: sibling prefixes, cached GenerateTask part; 8 levels only).  Each query
+// runs the smallest kernel holding its paths: a kernel's size is mostly code a given query
+// never runs, and the instruction-cache misses it causes cost 14-18 % on the rmat18 dense
+// queries (the pair-counting split).
+template <int D, bool ENUM, bool WORDS, int MODE>
 __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
+    constexpr bool SIB = MODE == kModePat;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t *wbase = smem_raw + (size_t)(threadIdx.x >> 5) * P.warp_stride;
     WarpStack<D> &S = *reinterpret_cast<WarpStack<D> *>(wbase);
@@ -1289,7 +1294,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
     const int last = (int)P.nq - 1;
     // this warp's sibling buffer (32 parent lanes x sib_cap words)
     const uint32_t sibL = SIB ? P.sib_level : 0u;
-    const uint32_t bulk_two = PAIR ? P.bulk_two : 0u;     // pair counting compiled in only when PAIR
+    const uint32_t bulk_two = MODE == kModePair ? P.bulk_two : 0u;    // (compiled in per MODE)
+    const uint32_t bulk_last = MODE != kModePlain ? P.bulk_last : 0u;
     const uint32_t sib_base = SIB ? (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u * P.sib_cap : 0u;
     Ctrl *C = P.ctrl;
     volatile Ctrl *VC = C;
@@ -1375,7 +1381,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 if (GM_GEN_CACHE && SIB && d0 + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, valid, lane, wacc);
                 if (d0 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, d0, valid, lane);
                 if (!ENUM && bulk_two && d0 == last - 2) prep_two<D>(P, S, scr, d0, valid, lane, wacc);
-                if (!ENUM && P.bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
+                if (!ENUM && bulk_last && d0 == last - 1) prep_last<D>(P, S, scr, d0, valid, lane, wacc);
                 base = d0; l = d0;
                 got = true;
                 break;
@@ -1410,7 +1416,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 if (GM_GEN_CACHE && SIB && (int)depth + 1 == (int)P.gen_level) gen_prep<D>(P, S, scr, lane == 0, lane, wacc);
                 if ((int)depth == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, depth, lane == 0, lane);
                 if (!ENUM && bulk_two && (int)depth == last - 2) prep_two<D>(P, S, scr, depth, lane == 0, lane, wacc);
-                if (!ENUM && P.bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
+                if (!ENUM && bulk_last && (int)depth == last - 1) prep_last<D>(P, S, scr, depth, lane == 0, lane, wacc);
                 base = (int)depth; l = (int)depth;
                 got = true;
                 break;
@@ -1512,7 +1518,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             // is then per task, without the warp-collective intersection)
             if (D >= GM_WIDE_MIN_D && !ENUM && l == (int)P.par_level &&
                 (bulk_two ? (GM_WIDE_PAIR && l == last - 2 && P.lab[last - 1] != P.lab[last])
-                            : (l == last || (P.bulk_last && l == last - 1)))) {
+                            : (l == last || (bulk_last && l == last - 1)))) {
                 constexpr int WT = D > 16 ? GM_WIDE_T32 : (D > 8 ? GM_WIDE_T16 : (SIB ? GM_WIDE_TSIB : GM_WIDE_T));
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
                 uint32_t tsrc[WT], toff[WT], k;
@@ -1710,7 +1716,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 __syncwarp();
                 continue;
             }
-            if (!ENUM && P.bulk_last && l == last - 1) {
+            if (!ENUM && bulk_last && l == last - 1) {
                 // last-level set counting: the extensions of this partial match are exactly the
                 // label-L(phi[last]) neighbours of its backward neighbour minus the mapped ones
                 if (F) add_count(my_count, count_last<D>(P, S, scr, l, v, src, wacc), ovf);
@@ -1740,7 +1746,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (SIB && l + 2 == (int)sibL) S.sibn[lane] = 0;        // new parents of level sib-1
             if (l + 1 == (int)P.par_level) prep_checks<D, SIB>(P, S, scr, l + 1, F, lane);
             if (!ENUM && bulk_two && l + 1 == last - 2) prep_two<D>(P, S, scr, l + 1, F, lane, wacc);
-            if (!ENUM && P.bulk_last && l + 1 == last - 1) prep_last<D>(P, S, scr, l + 1, F, lane, wacc);
+            if (!ENUM && bulk_last && l + 1 == last - 1) prep_last<D>(P, S, scr, l + 1, F, lane, wacc);
             if (lane == 0) { S.ci[l + 1] = 0; S.cj[l + 1] = 0; }
             __syncwarp();
             ++l;
@@ -1962,12 +1968,12 @@ static int ensure(uint32_t *&p, size_t &have, size_t need) {
 template <int D>
 static size_t stack_bytes() { return sizeof(WarpStack<D>); }
 
-template <int D, bool ENUM, bool WORDS, bool SIB = false, bool PAIR = false>
+template <int D, bool ENUM, bool WORDS, int MODE>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
     P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last + P.rows_gen));
     const size_t smem = (size_t)P.warp_stride * wpb;
-    auto kern = k_dfs<D, ENUM, WORDS, SIB, PAIR>;
+    auto kern = k_dfs<D, ENUM, WORDS, MODE>;
     GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int fit = 0;
     GM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, (int)(wpb * 32), smem));
@@ -2473,25 +2479,29 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         const uint32_t nq = p->nq;
         const bool cw = (o.flags & GM_FLAG_COUNT_WORDS) != 0;
         const uint32_t sharers = o.shared_pool_ctr ? o.world : 1u;
-#define GM_LAUNCH(DD, EE, WW, SS, PP) launch_dfs<DD, EE, WW, SS, PP>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
-#define GM_LAUNCH_WP(DD) (pair ? (cw ? GM_LAUNCH(DD, false, true, false, true) : GM_LAUNCH(DD, false, false, false, true)) \
-                               : (cw ? GM_LAUNCH(DD, false, true, false, false) : GM_LAUNCH(DD, false, false, false, false)))
-        const bool pair = P.bulk_two != 0;
+#define GM_LAUNCH(DD, EE, WW, MM) launch_dfs<DD, EE, WW, MM>(P, W.sms, o.warps_per_block, o.blocks_per_sm, sharers, st, &rs.grid, &rs.block)
+#define GM_LAUNCH_M(DD, MM) (cw ? GM_LAUNCH(DD, false, true, MM) : GM_LAUNCH(DD, false, false, MM))
+#define GM_LAUNCH_D(DD) (mode == kModePair ? GM_LAUNCH_M(DD, kModePair) : \
+                         (mode == kModeSet ? GM_LAUNCH_M(DD, kModeSet) : GM_LAUNCH_M(DD, kModePlain)))
+        // the smallest kernel that holds this query's paths (the enumerate kernels run every
+        // level by tasks: no counting code)
+        const int mode = (nq <= 8 && (P.sib_level || P.gen_level)) ? kModePat
+                       : (P.bulk_two ? kModePair : (P.bulk_last ? kModeSet : kModePlain));
         if (enumerate)   // (enumerate never counts words: its cost is the output)
-            rc = nq <= 8 ? GM_LAUNCH(8, true, false, false, false)
-                         : (nq <= 16 ? GM_LAUNCH(16, true, false, false, false) : GM_LAUNCH(32, true, false, false, false));
-        else if (nq <= 8 && (P.sib_level || P.gen_level))   // the 8-level pattern kernel (never pair counting)
-            rc = cw ? GM_LAUNCH(8, false, true, true, false) : GM_LAUNCH(8, false, false, true, false);
+            rc = nq <= 8 ? GM_LAUNCH(8, true, false, kModePlain)
+                         : (nq <= 16 ? GM_LAUNCH(16, true, false, kModePlain) : GM_LAUNCH(32, true, false, kModePlain));
         else if (nq <= 8)
-            rc = GM_LAUNCH_WP(8);
+            rc = mode == kModePat ? GM_LAUNCH_M(8, kModePat) : GM_LAUNCH_D(8);
         else if (nq <= 16)
-            rc = GM_LAUNCH_WP(16);
+            rc = GM_LAUNCH_D(16);
 #if GM_D24
         else if (nq <= 24)
-            rc = GM_LAUNCH_WP(24);
+            rc = GM_LAUNCH_D(24);
 #endif
         else
-            rc = GM_LAUNCH_WP(32);
+            rc = GM_LAUNCH_D(32);
+#undef GM_LAUNCH_D
+#undef GM_LAUNCH_M
 #undef GM_LAUNCH_WP
 #undef GM_LAUNCH
         if (rc) return rc;
