@@ -1278,8 +1278,8 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // their register budget and code size (the 8-level kernel spilled with it, and the other
 // queries lost 10-30 % to the larger code).
 // MODE: which counting code is compiled in -- kModePlain (none: every level by tasks),
-// kModeSet (last-level set counting), kModePair (set + pair counting), kModePat (set counting +
-// the pattern code: sibling prefixes, cached GenerateTask part; 8 levels only).  Each query
+// kModeSet (last-level set counting), kModePair (set + pair counting), kModePat (the pattern
+// code: sibling prefixes, cached GenerateTask part; 8 levels, no set counting).  Each query
 // runs the smallest kernel holding its paths: a kernel's size is mostly code a given query
 // never runs, and the instruction-cache misses it causes cost 14-18 % on the rmat18 dense
 // queries (the pair-counting split).
@@ -1295,7 +1295,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
     // this warp's sibling buffer (32 parent lanes x sib_cap words)
     const uint32_t sibL = SIB ? P.sib_level : 0u;
     const uint32_t bulk_two = MODE == kModePair ? P.bulk_two : 0u;    // (compiled in per MODE)
-    const uint32_t bulk_last = MODE != kModePlain ? P.bulk_last : 0u;
+    const uint32_t bulk_last = (MODE == kModeSet || MODE == kModePair) ? P.bulk_last : 0u;
     const uint32_t sib_base = SIB ? (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u * P.sib_cap : 0u;
     Ctrl *C = P.ctrl;
     volatile Ctrl *VC = C;
@@ -2440,7 +2440,8 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
             // the 5-cycle, +70 % embeddings in 5 s, and costs other queries)
             const uint32_t l = P.par_level;
             const uint32_t far = l != ~0u && l >= 2 ? (1u << (l - 1)) - 1 : 0u;
-            if (GM_GEN_CACHE && !(o.flags & GM_FLAG_NO_GEN_CACHE) && !enumerate && p->nq <= 8 && !P.sib_level && !P.bulk_two &&
+            if (GM_GEN_CACHE && !(o.flags & GM_FLAG_NO_GEN_CACHE) && !enumerate && p->nq <= 8 && !P.sib_level &&
+                !P.bulk_last && !P.bulk_two &&
                 far && (p->bw[l] & far) && ((P.sb_gt[l] | P.sb_lt[l]) & far)) {
                 P.gen_level = l;
                 P.rows_gen = 5;
