@@ -105,6 +105,9 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_HUB_SUMMARY
 #define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
 #endif
+#ifndef GM_TWO_VEC8
+#define GM_TWO_VEC8 0      // ... and 256-element rounds (two 16-byte loads, 8 probes per lane)
+#endif
 #ifndef GM_TWO_VEC
 #define GM_TWO_VEC 1       // pair-counting intersection: 128-element rounds with 16-byte loads
 #endif
@@ -1107,6 +1110,61 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
             while (true) {
                 // fast path: the cursor's list alone fills the round (long lists against a hub)
                 const uint32_t sl_ci = __shfl_sync(FULL, sl, ci & 31);
+#if GM_TWO_VEC8 && !GM_TWO_STAGE
+                if (ci < 32 && sl_ci - cj >= 256) {
+                    // 256 elements per round: two 16-byte loads per lane and 8 independent
+                    // probes in flight (the 128-element round below, twice as wide)
+                    const uint32_t f_sb = __shfl_sync(FULL, sb, ci), f_gb = __shfl_sync(FULL, gb, ci);
+                    const uint32_t f_ge = __shfl_sync(FULL, ge, ci), f_gown = __shfl_sync(FULL, gown, ci);
+                    const uint32_t start = f_sb + cj, a = start & ~3u;
+                    const uint4 q0 = __ldg(reinterpret_cast<const uint4 *>(P.nbr + a) + lane);
+                    const uint4 q1 = __ldg(reinterpret_cast<const uint4 *>(P.nbr + a + 128) + lane);
+                    const uint32_t x[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+                    bool hit[8];
+                    uint32_t nval = 0;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        hit[g] = a + 128 * (g >> 2) + 4 * lane + (g & 3) >= start;
+                        nval += hit[g];
+                    }
+                    words += nval;
+                    if (f_gown < P.nhubs) {
+                        const uint32_t *row = P.hub_bits + (unsigned long long)f_gown * P.hub_words;
+                        uint32_t wv[8];
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) wv[g] = hit[g] ? hub_summ_word<(D > 8)>(P, f_gown, x[g], words) : 0u;
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            hit[g] = hit[g] && summ_says(wv[g], x[g]);
+                            if (hit[g]) { wv[g] = ld_nc(row + (x[g] >> 5)); ++words; }
+                        }
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) hit[g] = hit[g] && ((wv[g] >> (x[g] & 31)) & 1u);
+                    } else {
+                        uint32_t n = f_ge - f_gb, b[8];
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) b[g] = f_gb;
+                        while (n > 1) {
+                            const uint32_t half = n >> 1;
+#pragma unroll
+                            for (int g = 0; g < 8; ++g) b[g] = (ld_nc(P.nbr + b[g] + half) <= x[g]) ? b[g] + half : b[g];
+                            n -= half;
+                            words += nval;
+                        }
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) hit[g] = hit[g] && n == 1 && ld_nc(P.nbr + b[g]) == x[g];
+                        words += nval;
+                    }
+                    uint32_t h = 0;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) h += __popc(__ballot_sync(FULL, hit[g]));
+                    if (lane == 0) S.tacc[ci] += h;
+                    __syncwarp();
+                    cj += a + 256 - start;
+                    if (cj == sl_ci) { ++ci; cj = 0; }
+                    continue;
+                }
+#endif
 #if GM_TWO_VEC
                 if (ci < 32 && sl_ci - cj >= 128) {
                     // 128 elements per round with one 16-byte load per lane (LDG.E.128): lane j
