@@ -107,7 +107,10 @@ GM_API int gm_graph_info(const gm_graph *g, gm_graph_info_t *info);
  * also gets a summary level: one bit per 256-vertex block of each bitmap (set iff the block
  * holds a neighbour), so most failing tests read an L2-resident summary word instead of a
  * DRAM sector of the bitmap.  summary: -1 = that rule, 0 = never (gm_load_graph's choice:
- * the extra dependent load measured 1-8 % slower on rmat24/26), 1 = always.  gm_load_graph builds it with
+ * the extra dependent load measured 1-8 % slower on rmat24/26), 1 = always.
+ * The search kernels read the summary only in a build with GM_HUB_SUMMARY=1 (the default
+ * build compiles the test out: 3-52 % more tasks/s on rmat24/26); without it a summary is
+ * built but unused.  gm_load_graph builds it with
  * min_degree 64 and a 64 MiB budget when the CSR fits in L2 beside it, else an 8 GiB budget
  * (at most a quarter of the free device memory); budget_bytes = 0 removes it.  Results
  * never depend on it.

@@ -103,8 +103,8 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #define GM_WIDE_T32 4      // ... in the 32-level kernel (4 vs 2: rmat26 +4 to +23 % tasks/s)
 #endif
 #ifndef GM_HUB_SUMMARY
-#define GM_HUB_SUMMARY 1   // use the hub index's summary level when the graph has one
-#endif
+#define GM_HUB_SUMMARY 0   // 1: the kernels use the hub index's summary level when the graph has one
+#endif                     // (0: the test is compiled out -- rmat24 +17-19 %, rmat26 +3-52 % tasks/s)
 #ifndef GM_TWO_VEC8
 #define GM_TWO_VEC8 0      // ... and 256-element rounds (two 16-byte loads, 8 probes per lane)
 #endif
