@@ -131,6 +131,10 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_GEN_CACHE
 #define GM_GEN_CACHE 1     // GenerateTask at the hot level with a per-grandparent cached part (gen_prep)
 #endif
+#ifndef GM_TEAM_CODE
+#define GM_TEAM_CODE 1     // (A/B switch) 0 compiles the cross-GPU stealing team code out of the kernels
+#endif
+#define GM_TEAMN(P) (GM_TEAM_CODE ? (P).team_n : 0u)
 #ifndef GM_CUT_MIN
 #define GM_CUT_MIN 0       // GenerateTask under symmetry-breaking bounds: the backward row with the
 #endif                     // fewest candidates INSIDE the bounds (else: the shortest row, then cut)
@@ -366,16 +370,16 @@ __device__ __forceinline__ unsigned long long ld_sys64(const unsigned long long 
 // epoch holds no unit of this search (the rank has not started it, or has finished it, which
 // needs its lineage count at zero), so consecutive searches need no barrier between them.
 __device__ __forceinline__ void work_add(const SearchParams &P, Ctrl *C, uint32_t home, int delta) {
-    if (P.team_n) atomicAdd_system(&P.team_ctrl[home]->tword, (unsigned long long)(long long)delta);
+    if (GM_TEAMN(P)) atomicAdd_system(&P.team_ctrl[home]->tword, (unsigned long long)(long long)delta);
     else atomicAdd(&C->work, delta);
 }
 __device__ __forceinline__ int req_add(const SearchParams &P, Ctrl *C, int delta) {
-    return P.team_n ? atomicAdd_system(&C->requests, delta) : atomicAdd(&C->requests, delta);
+    return GM_TEAMN(P) ? atomicAdd_system(&C->requests, delta) : atomicAdd(&C->requests, delta);
 }
 // every rank's lineage count is zero (the whole team is out of work)
 __device__ __forceinline__ bool team_idle(const SearchParams &P, volatile Ctrl *VC) {
-    if (!P.team_n) return VC->work == 0;
-    for (uint32_t r = 0; r < P.team_n; ++r) {
+    if (!GM_TEAMN(P)) return VC->work == 0;
+    for (uint32_t r = 0; r < GM_TEAMN(P); ++r) {
         const unsigned long long w = ld_sys64(&P.team_ctrl[r]->tword);
         if ((uint32_t)(w >> 32) == P.epoch && (uint32_t)w != 0) return false;
     }
@@ -383,7 +387,7 @@ __device__ __forceinline__ bool team_idle(const SearchParams &P, volatile Ctrl *
 }
 // Pop one item from rank r's ring (r = this rank: its own ring); returns its position or ~0.
 __device__ __forceinline__ unsigned long long ring_pop(const SearchParams &P, Ctrl *C, uint32_t r) {
-    if (!P.team_n) {
+    if (!GM_TEAMN(P)) {
         volatile Ctrl *VC = C;
         const unsigned long long pos = VC->q_head;
         const unsigned long long seq = ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
@@ -1403,13 +1407,13 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         // then (team) the other ranks' rings over peer memory
                         item = ring_pop(P, C, P.team_rank);
                         src_rank = P.team_rank;
-                        for (uint32_t k = 1; k < P.team_n && item == ~0ull; ++k) {
-                            src_rank = (P.team_rank + k) % P.team_n;
+                        for (uint32_t k = 1; k < GM_TEAMN(P) && item == ~0ull; ++k) {
+                            src_rank = (P.team_rank + k) % GM_TEAMN(P);
                             item = ring_pop(P, C, src_rank);
                         }
-                        if (item == ~0ull && P.team_n > 1 && (++idle_polls & 31u) == 0) {
+                        if (item == ~0ull && GM_TEAMN(P) > 1 && (++idle_polls & 31u) == 0) {
                             // still idle: ask the next rank's busy warps to split their stacks
-                            const uint32_t r = (P.team_rank + 1 + (idle_polls >> 5) % (P.team_n - 1)) % P.team_n;
+                            const uint32_t r = (P.team_rank + 1 + (idle_polls >> 5) % (GM_TEAMN(P) - 1)) % GM_TEAMN(P);
                             atomicAdd_system(&P.team_ctrl[r]->requests, 1);
                         }
                         if (item == ~0ull && pool_peek(P) >= P.pool_size && team_idle(P, VC))
@@ -1447,13 +1451,13 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             if (item != ~0ull) {
                 // lane 0's acquire load of the slot's sequence number, then this warp barrier
                 // (memory-ordering among the lanes), then every lane's strong item loads
-                if (P.team_n) __threadfence_system(); else __threadfence();
+                if (GM_TEAMN(P)) __threadfence_system(); else __threadfence();
                 __syncwarp();
                 const unsigned long long slot = item % P.q_cap;
                 // written by another SM (or, in a team, another GPU): volatile loads, which
                 // are strong at system scope (LDG.E.STRONG.SYS), never a stale L1 line
                 const volatile uint32_t *it =
-                    (P.team_n ? P.team_items[src_rank] : P.q_items) + slot * kItemWords;
+                    (GM_TEAMN(P) ? P.team_items[src_rank] : P.q_items) + slot * kItemWords;
                 const uint32_t depth = it[0];
                 if (lane < depth) { S.v[lane][0] = it[6 + lane]; S.pid[lane][0] = 0; }
                 S.cb[depth][lane] = lane == 0 ? it[1] : 0;
@@ -1462,7 +1466,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 if (lane == 0) S.home = it[4];
                 __syncwarp();
                 if (lane == 0) {   // release the slot for the next lap of the ring
-                    if (P.team_n) {
+                    if (GM_TEAMN(P)) {
                         __threadfence_system();
                         ((volatile unsigned long long *)P.team_seq[src_rank])[slot] = item + P.q_cap;
                     } else {
@@ -1494,7 +1498,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     if (P.limit_ns && globaltimer() > VC->t0 + P.limit_ns) atomicExch(&C->abort, 1);
                     ab = VC->abort;
                     // work stealing (§4.3): serve one posted request by splitting our stack
-                    if (P.steal && (P.team_n ? ld_sys(&C->requests) : VC->requests) > 0) {
+                    if (P.steal && (GM_TEAMN(P) ? ld_sys(&C->requests) : VC->requests) > 0) {
                         if (req_add(P, C, -1) > 0) claim = 1;
                         else req_add(P, C, 1);
                     }
@@ -1532,7 +1536,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                             pos = VC->q_tail;
                             while (true) {
                                 // (slots are released by poppers, possibly on other GPUs)
-                                const unsigned long long seq = P.team_n ? ld_acq_sys(P.q_seq + pos % P.q_cap)
+                                const unsigned long long seq = GM_TEAMN(P) ? ld_acq_sys(P.q_seq + pos % P.q_cap)
                                                                         : ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap];
                                 if (seq == pos) {
                                     const unsigned long long prev = atomicCAS(&C->q_tail, pos, pos + 1);
@@ -1555,7 +1559,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                             it[4] = S.home; it[5] = P.epoch;
                             read_prefix<D>(S, s - 1, giver, it + 6);
                             S.cl[s][giver] = mask ? 0u : gb;
-                            if (P.team_n) __threadfence_system(); else __threadfence();
+                            if (GM_TEAMN(P)) __threadfence_system(); else __threadfence();
                             ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap] = pos + 1;
                         }
                         served = 1;
