@@ -131,6 +131,9 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #ifndef GM_GEN_CACHE
 #define GM_GEN_CACHE 1     // GenerateTask at the hot level with a per-grandparent cached part (gen_prep)
 #endif
+#ifndef GM_PREFETCH_ROWS
+#define GM_PREFETCH_ROWS 0 // prefetch the task vertex's row offsets for the counting step (A/B)
+#endif
 #ifndef GM_TEAM_CODE
 #define GM_TEAM_CODE 1     // (A/B switch) 0 compiles the cross-GPU stealing team code out of the kernels
 #endif
@@ -1645,6 +1648,20 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
                 my_rounds += (lane == 0) ? (uint32_t)WT : 0u;   // 32 WT task slots (idle rate)
                 my_tasks += nh;
+#if GM_PREFETCH_ROWS
+                // the counting step after the checks reads the task vertex's own row offsets (pair
+                // counting with a leaf on this level, set counting with phi[last]'s backward
+                // neighbour on it): start those loads now so they overlap the checks
+                if (bulk_two || bulk_last) {
+                    const uint32_t pl = bulk_two ? ((int)P.two_b6 == l ? P.lab[l + 1] : ((int)P.two_b7 == l ? P.lab[l + 2] : ~0u))
+                                                 : ((int)P.last_b == l ? P.lab[l + 1] : ~0u);
+                    if (pl != ~0u) {
+#pragma unroll
+                        for (int t = 0; t < WT; ++t)
+                            if (th[t]) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.offs + tv[t] * P.S + pl));
+                    }
+                }
+#endif
                 process_parT<D, WT, SIB>(P, S, scr, l, tv, tsrc, th, tf, wacc);
 #ifdef GM_LEVEL_STATS
                 {
