@@ -25,7 +25,9 @@
  *     borrows its graph: free plans before their graph.
  *   - Vertex ids are uint32 in [0, n); labels are uint32 in [0, num_labels).
  *   - Limits: n * num_labels < 2^32, stored adjacency entries < 2^32,
- *     query size 1 <= nq <= GM_MAX_QUERY.  Exceeding a limit returns GM_ERR_LIMIT.
+ *     query size 1 <= nq <= GM_MAX_QUERY, and (gm_count / gm_enumerate) maximum degree
+ *     < 2^27 (a DFS stack entry packs a slice length with its source level).
+ *     Exceeding a limit returns GM_ERR_LIMIT.
  */
 #ifndef GMATCH_H
 #define GMATCH_H
@@ -206,7 +208,10 @@ typedef struct {
     uint32_t root_chunk;     /* 0 = 64 */
     uint32_t steal;          /* 1 = idle-warp work stealing on (gm_default_opts), 0 = off */
     uint32_t blocks_per_sm;  /* 0 = as many as fit */
-    uint32_t warps_per_block;/* DFS warps per block, 1..4 (0 = 4); larger: GM_ERR_ARG */
+    uint32_t warps_per_block;/* DFS warps per block: 0 (default) = the block size that keeps
+                                the most warps resident for this query's shared memory; else
+                                1..4 (<= 8-vertex queries) or 1..14 (larger ones); more:
+                                GM_ERR_ARG; a block over 227 KB: GM_ERR_LIMIT */
     double   time_limit_ms;  /* 0 = none; on expiry the call returns GM_TIMEOUT */
     const uint32_t *roots;   /* optional host list of DISTINCT vertices restricting phi[0]'s
                                 images to them (still filtered and rank-partitioned);

@@ -27,6 +27,8 @@
 //    from busy warps by splitting the execution stack", via a ring instead of a direct
 //    warp-to-warp hand-off.  Termination: `work` counts warps holding work plus items in
 //    the ring; a warp exits when the pool is exhausted and work == 0.
+#include <stddef.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -47,6 +49,9 @@ constexpr uint32_t FULL = 0xffffffffu;
 #define CHK(k, x) scr[(k) * 32u + (x)]
 #define LASTW(k, x) scr[(P.rows_chk + (k)) * 32u + (x)]
 #define GENW(k, x) scr[(P.rows_chk + P.rows_last + (k)) * 32u + (x)]   // gen_prep's cached slice
+// then rows_aux rows of per-lane counting state (set / pair counting kernels only):
+// 0 lastmb, 1 lastlb, 2 lastub (prep_last / prep_two), 3 tacc (pair counting)
+#define AUXW(k, x) scr[(P.aux_row + (k)) * 32u + (x)]
 #ifndef GM_CHK_ORDER
 #define GM_CHK_ORDER 1
 #endif
@@ -59,13 +64,17 @@ constexpr uint32_t FULL = 0xffffffffu;
 #ifndef GM_DFS_MINB
 #define GM_DFS_MINB 9      // resident 128-thread blocks per SM for the 8-level kernel (<= 56 registers)
 #endif
-// 16/32-level kernels: the WarpStack (7.8 / 15.6 KB per warp) limits residency to ~6 / ~3 blocks
-// per SM, so they may use the registers that frees
+// 16/24/32-level kernels: shared memory (the stack, 6-15 KB per warp) limits their residency,
+// so they are compiled for blocks of up to GM_WPB_WIDE warps at 72 registers (28 warps per
+// SM), and the host picks, per query, the block size that keeps the most warps resident
+#ifndef GM_WPB_WIDE
+#define GM_WPB_WIDE 14
+#endif
 #ifndef GM_MINB16
-#define GM_MINB16 7
+#define GM_MINB16 (28 / GM_WPB_WIDE)
 #endif
 #ifndef GM_MINB32
-#define GM_MINB32 7
+#define GM_MINB32 (28 / GM_WPB_WIDE)
 #endif
 #define GM_DFS_MINB_D(D) ((D) <= 8 ? GM_DFS_MINB : ((D) <= 16 ? GM_MINB16 : GM_MINB32))
 #ifndef GM_TWO_STAGE
@@ -138,14 +147,21 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #define GM_TEAM_CODE 1     // (A/B switch) 0 compiles the cross-GPU stealing team code out of the kernels
 #endif
 #define GM_TEAMN(P) (GM_TEAM_CODE ? (P).team_n : 0u)
+#ifndef GM_PACK_CS
+#define GM_PACK_CS 1       // the slice's source level in the top 5 bits of its length (416-byte levels)
+#endif
 #ifndef GM_CUT_MIN
 #define GM_CUT_MIN 0       // GenerateTask under symmetry-breaking bounds: the backward row with the
 #endif                     // fewest candidates INSIDE the bounds (else: the shortest row, then cut)
-constexpr uint32_t kDfsMaxWarps = 4;   // k_dfs is compiled for 128-thread blocks (__launch_bounds__)
+constexpr uint32_t kDfsMaxWarps = GM_WPB_WIDE > 4 ? GM_WPB_WIDE : 4;   // largest k_dfs block, any D
+// warps per block k_dfs<D> is compiled for (__launch_bounds__): 4 for the register-limited
+// 8-level kernels, GM_WPB_WIDE for the shared-memory-limited deeper ones
+template <int D>
+constexpr uint32_t dfs_max_warps() { return D <= 8 ? 4u : (uint32_t)GM_WPB_WIDE; }
 constexpr uint32_t kItemWords = 6 + kMaxQ;     // [depth, cb, cl, cs, home, epoch, prefix[kMaxQ]]
 constexpr uint32_t kMaxTeam = 8;               // ranks of a stealing team (gm_team)
 constexpr int kModePlain = 0, kModeSet = 1, kModePair = 2, kModePat = 3;   // k_dfs MODE
-constexpr uint8_t kSibCs = 0xff;               // WarpStack.cs of a slice in the sibling buffer
+constexpr uint32_t kSibCs = GM_PACK_CS ? 31u : 0xffu;   // source level of a slice in the sibling buffer
 constexpr uint32_t kSibCap = 256;              // sibling-prefix entries per parent lane
 
 // Global control block.  Every field that many warps poll or update lives on its own
@@ -224,6 +240,10 @@ struct SearchParams {
     uint32_t gen_level;         // GenerateTask of this level uses gen_prep's per-grandparent slice (0: off)
     uint32_t rows_gen;          // scratch rows for it (5 or 0)
     uint32_t warp_stride;       // bytes of shared memory per warp: WarpStack + scratch rows
+    uint32_t levels;            // stack levels allocated per warp (WarpStack.lv[0 .. levels))
+    uint32_t rows_aux;          // scratch rows of counting state (AUXW): 3 set counting, 4 pair, else 0
+    uint32_t aux_row;           // their first row: rows_chk + rows_last + rows_gen
+    uint32_t stack_bytes;       // header + levels * sizeof(StackLevel): the scratch rows start there
     uint32_t par_level;         // level whose checks are kept per parent (prep_checks), or ~0u
     uint32_t par_low;           // deepest level prep_checks visits
     uint32_t *out;              // enumerate rows (nq words each)
@@ -433,24 +453,47 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// One level l of a warp's DFS stack (§4.2, Alg. 2 S[l][lane]): 448 bytes, or 416 with the
+// slice length and source level packed in one word (GM_PACK_CS: lengths < 2^27, a row
+// bound gm_count checks; source levels < 31, and 31 marks a sibling-buffer slice).
+struct alignas(16) StackLevel {
+    uint32_t v[32];       // S[l][lane].v   : candidate data vertex of the task in this lane
+    uint32_t cb[32];      // S[l][lane].C   : begin of the local candidate slice of lane's partial match
+#if GM_PACK_CS
+    uint32_t clcs[32];    //                  its length | (source level << 27)
+#else
+    uint32_t cl[32];      //                  its length
+    uint8_t cs[32];       //                  level whose vertex produced the slice (its check is implied)
+#endif
+    uint8_t pid[32];      // S[l][lane].pid : parent lane at level l-1
+#if GM_PACK_CS
+    static constexpr uint32_t kClMask = (1u << 27) - 1;
+    __device__ __forceinline__ uint32_t len(uint32_t j) const { return clcs[j] & kClMask; }
+    __device__ __forceinline__ uint32_t src(uint32_t j) const { return clcs[j] >> 27; }
+    __device__ __forceinline__ void set(uint32_t j, uint32_t n, uint32_t s) { clcs[j] = n | (s << 27); }
+    __device__ __forceinline__ void set_len(uint32_t j, uint32_t n) { clcs[j] = (clcs[j] & ~kClMask) | n; }
+#else
+    __device__ __forceinline__ uint32_t len(uint32_t j) const { return cl[j]; }
+    __device__ __forceinline__ uint32_t src(uint32_t j) const { return cs[j]; }
+    __device__ __forceinline__ void set(uint32_t j, uint32_t n, uint32_t s) { cl[j] = n; cs[j] = (uint8_t)s; }
+    __device__ __forceinline__ void set_len(uint32_t j, uint32_t n) { cl[j] = n; }
+#endif
+};
+
+// A warp's shared-memory state: a fixed header, then the stack levels.  Only the levels a
+// query's search touches are allocated (SearchParams.levels, host-computed: the counted
+// last one or two levels of set / pair counting hold nothing), and the per-warp scratch rows
+// -- check images and set/pair-counting words, sized per query (SearchParams.rows_chk /
+// rows_last) -- follow them: so a query of fewer than D vertices, or one that counts its
+// last levels, keeps more warps resident on the shared-memory-limited 16/24/32-level kernels.
 template <int D>
 struct alignas(16) WarpStack {
-    uint32_t v[D][32];    // S[l][lane].v   : candidate data vertex of the task in this lane
-    uint32_t cb[D][32];   // S[l][lane].C   : begin of the local candidate slice of lane's partial match
-    uint32_t cl[D][32];   //                  its length
-    uint8_t pid[D][32];   // S[l][lane].pid : parent lane at level l-1
-    uint8_t cs[D][32];    //                  level whose vertex produced the slice (its check is implied)
-    // (the per-warp scratch rows -- check images and set/pair-counting words -- follow the
-    // struct in shared memory, sized per query: see SearchParams.rows_chk / rows_last)
-    uint32_t lastmb[32];  //               and the image of phi[last]'s backward neighbour (if < last-1)
-    uint32_t lastlb[32];  //               symmetry-breaking bounds of phi[last] from levels < last-1:
-    uint32_t lastub[32];  //               its image must lie in [lastlb, lastub)
-    uint32_t tacc[32];    // pair counting: per-lane |A n R| accumulators
     unsigned long long mbar;  // GM_TWO_STAGE: mbarrier of the warp's bulk-copy staging buffer
     uint32_t home;            // gm_team: lineage rank of the unit this warp holds
-    uint32_t sibn[32];        // sibling prefixes: siblings recorded so far per parent lane
+    uint32_t sibn[D <= 8 ? 32 : 1];   // sibling prefixes (8-level kernels only): siblings per parent lane
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
+    StackLevel lv[D];     // levels 0 .. SearchParams.levels - 1 are allocated
 };
 
 // GenerateTask (Alg. 2 lines 17-24, Erratum 2 read as a running minimum): the local
@@ -474,15 +517,15 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
             // row (a low-degree vertex's neighbours are mostly high-degree, i.e. small ids).
             // First the bounds, then each row's cut by two binary searches.
             for (int i = l - 1; i >= lowest; --i) {
-                const uint32_t w = S.v[i][p];
+                const uint32_t w = S.lv[i].v[p];
                 if ((gt >> i) & 1u) lb = max(lb, w + 1);
                 if ((lt >> i) & 1u) ub = min(ub, w);
-                p = S.pid[i][p];
+                p = S.lv[i].pid[p];
             }
             p = lane;
             for (int i = l - 1; i >= lowest; --i) {
                 if ((bw >> i) & 1u) {
-                    const uint32_t row = S.v[i][p] * P.S + lab;
+                    const uint32_t row = S.lv[i].v[p] * P.S + lab;
                     const uint32_t lo = ld_nc(P.offs + row), len = ld_nc(P.offs + row + 1) - lo;
                     words += 2;
                     if (lb < ub && len) {
@@ -493,11 +536,11 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
                         best = 0; cb = lo; cs = (uint32_t)i;
                     }
                 }
-                p = S.pid[i][p];
+                p = S.lv[i].pid[p];
             }
         } else {
             for (int i = l - 1; i >= lowest; --i) {
-                const uint32_t w = S.v[i][p];
+                const uint32_t w = S.lv[i].v[p];
                 if ((bw >> i) & 1u) {
                     const uint32_t row = w * P.S + lab;
                     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
@@ -506,7 +549,7 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
                 }
                 if ((gt >> i) & 1u) lb = max(lb, w + 1);
                 if ((lt >> i) & 1u) ub = min(ub, w);
-                p = S.pid[i][p];
+                p = S.lv[i].pid[p];
             }
             if (gt | lt) {   // the slice is sorted: cut it to the ids the conditions allow
                 uint32_t a = 0, e = best;
@@ -517,9 +560,8 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
             }
         }
     }
-    S.cb[l][lane] = cb;
-    S.cl[l][lane] = best;
-    S.cs[l][lane] = (uint8_t)cs;
+    S.lv[l].cb[lane] = cb;
+    S.lv[l].set(lane, best, cs);
 }
 
 // GenerateTask with a per-grandparent part (GM_GEN_CACHE).  At level l = P.gen_level (the
@@ -544,7 +586,7 @@ __device__ __forceinline__ void gen_prep(const SearchParams &P, WarpStack<D> &S,
     const int lowest = __ffs(bw | gt | lt) - 1;
     uint32_t p = lane;
     for (int i = l - 2; i >= lowest && lowest >= 0; --i) {
-        const uint32_t w = S.v[i][p];
+        const uint32_t w = S.lv[i].v[p];
         if ((bw >> i) & 1u) {
             const uint32_t row = w * P.S + lab;
             const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
@@ -553,7 +595,7 @@ __device__ __forceinline__ void gen_prep(const SearchParams &P, WarpStack<D> &S,
         }
         if ((gt >> i) & 1u) lb = max(lb, w + 1);
         if ((lt >> i) & 1u) ub = min(ub, w);
-        p = S.pid[i][p];
+        p = S.lv[i].pid[p];
     }
     if (bw && (gt | lt)) {
         uint32_t a = 0, e = best;
@@ -570,8 +612,8 @@ __device__ __forceinline__ void generate_cached(const SearchParams &P, WarpStack
                                                 bool valid, uint32_t lane, uint32_t &words) {
     uint32_t best = 0, cb = 0, cs = 0;
     if (valid) {
-        const uint32_t p = S.pid[l - 1][lane];
-        const uint32_t v1 = S.v[l - 1][lane];
+        const uint32_t p = S.lv[l - 1].pid[lane];
+        const uint32_t v1 = S.lv[l - 1].v[lane];
         const uint32_t nb = (P.bw[l] >> (l - 1)) & 1u;
         const uint32_t ngt = (P.sb_gt[l] >> (l - 1)) & 1u, nlt = (P.sb_lt[l] >> (l - 1)) & 1u;
         cb = GENW(0, p); best = GENW(1, p); cs = GENW(2, p);
@@ -600,9 +642,8 @@ __device__ __forceinline__ void generate_cached(const SearchParams &P, WarpStack
             best = e > a ? e - a : 0;
         }
     }
-    S.cb[l][lane] = cb;
-    S.cl[l][lane] = best;
-    S.cs[l][lane] = (uint8_t)cs;
+    S.lv[l].cb[lane] = cb;
+    S.lv[l].set(lane, best, cs);
 }
 
 // Process (Alg. 2 lines 32-41, Erratum 1 read as "lanes without a task return false"):
@@ -625,7 +666,7 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         ++words;
     }
     bool ok = has;
-    const uint32_t cs = has ? S.cs[l][src] : 0u;
+    const uint32_t cs = has ? S.lv[l].src(src) : 0u;
     const uint32_t chk = has ? P.bw[l] & ~(1u << cs) : 0u;   // exactly nchk images for a task
     const uint32_t lab = P.lab[l];
     // Only levels holding a backward neighbour (adjacency check) or a vertex of v's label
@@ -647,12 +688,12 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         // (ordering hub checks first measured 1-7 % slower on rmat18 dense queries: pairs of
         // mixed hub/search probes overlap better)
         for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
-            const uint32_t w = S.v[i][p];
+            const uint32_t w = S.lv[i].v[p];
             if ((eq >> i) & 1u) ok = ok && (w != v);
             if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
             if ((lt >> i) & 1u) ok = ok && (v < w);
             if ((chk >> i) & 1u) { CHK(k, lane) = w; ++k; }
-            p = S.pid[i][p];
+            p = S.lv[i].pid[p];
         }
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
@@ -832,17 +873,17 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
     // to its backward images, injectivity against the same-label images below, its bounds --
     // so only the positions in sib_chk remain; unused rows hold ~0u ("no check": no vertex has
     // that id, process() skips it and injectivity never matches it)
-    const bool sibl = SIB && (uint32_t)l == P.sib_level && S.cs[l][lane] == kSibCs;
-    const uint32_t chkm = sibl ? P.sib_chk : P.bw[l] & ~(1u << S.cs[l][lane]);
+    const bool sibl = SIB && (uint32_t)l == P.sib_level && S.lv[l].src(lane) == kSibCs;
+    const uint32_t chkm = sibl ? P.sib_chk : P.bw[l] & ~(1u << S.lv[l].src(lane));
     const uint32_t eqm = sibl ? 0u : P.same_lab[l] & ~P.bw[l];
     const int nchk = __popc(P.bw[l]) - 1;
     int kc = 0, ke = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.par_low; --i) {
-        const uint32_t w = S.v[i][p];
+        const uint32_t w = S.lv[i].v[p];
         if ((chkm >> i) & 1u) { CHK(kc, lane) = w; ++kc; }
         if ((eqm >> i) & 1u) { CHK(nchk + ke, lane) = w; ++ke; }
-        p = S.pid[i][p];
+        p = S.lv[i].pid[p];
     }
     if (SIB && P.sib_level) {
         for (int k = kc; k < nchk; ++k) CHK(k, lane) = ~0u;
@@ -896,8 +937,8 @@ __device__ __forceinline__ uint32_t sib_append(const SearchParams &P, WarpStack<
 // the warp's sibling buffer -- written during this launch, so read with a coherent load
 template <int D, bool SIB>
 __device__ __forceinline__ uint32_t cand_at(const SearchParams &P, const WarpStack<D> &S, int l, uint32_t src, uint32_t off) {
-    const uint32_t cb = S.cb[l][src];
-    if (SIB && P.sib_level == (uint32_t)l && S.cs[l][src] == kSibCs) return P.sib[cb + off];
+    const uint32_t cb = S.lv[l].cb[src];
+    if (SIB && P.sib_level == (uint32_t)l && S.lv[l].src(src) == kSibCs) return P.sib[cb + off];
     return ld_nc(P.nbr + cb + off);
 }
 
@@ -925,17 +966,17 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     int k = 0, ka = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.last_low; --i) {
-        const uint32_t w = S.v[i][p];
+        const uint32_t w = S.lv[i].v[p];
         if (i == b) mb = w;
         if ((test >> i) & 1u) { LASTW(k, lane) = w; ++k; }
         if ((known >> i) & 1u) { LASTW(P.last_k + ka, lane) = w; ++ka; }
         if ((gt >> i) & 1u) lb = max(lb, w + 1);
         if ((lt >> i) & 1u) ub = min(ub, w);
-        p = S.pid[i][p];
+        p = S.lv[i].pid[p];
     }
-    S.lastmb[lane] = mb;
-    S.lastlb[lane] = lb;
-    S.lastub[lane] = ub;
+    AUXW(0, lane) = mb;
+    AUXW(1, lane) = lb;
+    AUXW(2, lane) = ub;
     if (b < l && !P.last_sb) {
         // M[b] is fixed for this parent: the count of every task is this constant minus (at
         // most) the task's own vertex; keep it in lastlb (bounds are unused without SB)
@@ -946,7 +987,7 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
         words += 2;
         for (int c = 0; c < k; ++c)
             if (has_edge<(D > 8)>(P, mb, P.lab[b], LASTW(c, lane), lab, words)) --cnt;
-        S.lastlb[lane] = cnt;
+        AUXW(1, lane) = cnt;
     }
 }
 
@@ -955,10 +996,10 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
                                                uint32_t src, uint32_t &words) {
     const uint32_t lab = P.lab[l + 1];
     const uint32_t same = P.last_same;    // positions i < last, i != b, with L(phi[i]) == lab
-    const uint32_t mb = (int)P.last_b == l ? v : S.lastmb[src];   // M[b]
+    const uint32_t mb = (int)P.last_b == l ? v : AUXW(0, src);   // M[b]
     const uint32_t lb_lab = P.lab[P.last_b];                       // L(M[b])
     if (!P.last_sb && (int)P.last_b < l) {   // parent-constant part precomputed by prep_last
-        uint32_t cnt = S.lastlb[src];
+        uint32_t cnt = AUXW(1, src);
         if (((same >> l) & 1u) && !((P.last_adj >> l) & 1u) && has_edge<(D > 8)>(P, mb, lb_lab, v, lab, words)) --cnt;
         return cnt;
     }
@@ -968,7 +1009,7 @@ __device__ __forceinline__ uint32_t count_last(const SearchParams &P, const Warp
     if (P.last_sb) {
         // symmetry breaking bounds phi[last]'s image to [lb, ub): count that part of the sorted
         // slice, then remove the mapped same-label vertices inside it
-        uint32_t lb = S.lastlb[src], ub = S.lastub[src];
+        uint32_t lb = AUXW(1, src), ub = AUXW(2, src);
         if ((P.sb_gt[l + 1] >> l) & 1u) lb = max(lb, v + 1);
         if ((P.sb_lt[l + 1] >> l) & 1u) ub = min(ub, v);
         if (lb >= ub) return 0;
@@ -1010,10 +1051,10 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
     uint32_t m6 = 0, m7 = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.two_low; --i) {
-        const uint32_t w = S.v[i][p];
+        const uint32_t w = S.lv[i].v[p];
         if (i == b6) m6 = w;
         if (i == b7) m7 = w;
-        p = S.pid[i][p];
+        p = S.lv[i].pid[p];
     }
     LASTW(0, lane) = m6;
     LASTW(1, lane) = m7;
@@ -1031,17 +1072,17 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
     if (!P.two_walk) {
         p = lane;
         for (int i = l - 1; i >= (int)P.two_low; --i) {
-            const uint32_t w = S.v[i][p];
+            const uint32_t w = S.lv[i].v[p];
             bool a = false, r = false;
             if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], w, lab6, words);
             if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], w, lab7, words);
             inA += a; inR += r; inAR += a && r;
-            p = S.pid[i][p];
+            p = S.lv[i].pid[p];
         }
     }
-    S.lastmb[lane] = inA;
-    S.lastlb[lane] = inR;
-    S.lastub[lane] = inAR;
+    AUXW(0, lane) = inA;
+    AUXW(1, lane) = inR;
+    AUXW(2, lane) = inAR;
 }
 
 // Pair counting (count mode): when phi[last-1] and phi[last] each
@@ -1077,15 +1118,15 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
         if (P.two_walk) {       // a per-task row with same-label images below l: test them all here
             uint32_t p = src;
             for (int i = l - 1; i >= (int)P.two_low; --i) {
-                const uint32_t w = S.v[i][p];
+                const uint32_t w = S.lv[i].v[p];
                 bool a = false, r = false;
                 if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], w, lab6, words);
                 if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], w, lab7, words);
                 inA += a; inR += r; inAR += a && r;
-                p = S.pid[i][p];
+                p = S.lv[i].pid[p];
             }
         } else {                // every image below l was tested once per parent
-            inA = S.lastmb[src]; inR = S.lastlb[src]; inAR = S.lastub[src];
+            inA = AUXW(0, src); inR = AUXW(1, src); inAR = AUXW(2, src);
         }
         {   // the task's own vertex (never in a row it owns: same6/same7 exclude b6/b7)
             bool a = false, r = false;
@@ -1107,7 +1148,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
             const bool a_short = a1 - a0 <= r1 - r0;
             const uint32_t sb = a_short ? a0 : r0, sl = F ? (a_short ? a1 - a0 : r1 - r0) : 0u;
             const uint32_t gb = a_short ? r0 : a0, ge = a_short ? r1 : a1, gown = a_short ? m7 : m6;
-            S.tacc[lane] = 0;
+            AUXW(3, lane) = 0;
             __syncwarp();
             uint32_t ci = 0, cj = 0;
 #if GM_TWO_STAGE
@@ -1165,7 +1206,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     uint32_t h = 0;
 #pragma unroll
                     for (int g = 0; g < 8; ++g) h += __popc(__ballot_sync(FULL, hit[g]));
-                    if (lane == 0) S.tacc[ci] += h;
+                    if (lane == 0) AUXW(3, ci) += h;
                     __syncwarp();
                     cj += a + 256 - start;
                     if (cj == sl_ci) { ++ci; cj = 0; }
@@ -1240,7 +1281,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     uint32_t h = 0;
 #pragma unroll
                     for (int g = 0; g < 4; ++g) h += __popc(__ballot_sync(FULL, hit[g]));
-                    if (lane == 0) S.tacc[ci] += h;
+                    if (lane == 0) AUXW(3, ci) += h;
                     __syncwarp();
                     cj += a + 128 - start;
                     if (cj == sl_ci) { ++ci; cj = 0; }
@@ -1271,7 +1312,7 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                         if (step == 64) hit2 = contains(P.nbr, f_gb, f_ge, x2, words);
                     }
                     const uint32_t h = __popc(__ballot_sync(FULL, hit)) + __popc(__ballot_sync(FULL, hit2));
-                    if (lane == 0) S.tacc[ci] += h;
+                    if (lane == 0) AUXW(3, ci) += h;
                     __syncwarp();
                     cj += step;
                     if (cj == sl_ci) { ++ci; cj = 0; }
@@ -1311,11 +1352,11 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
                     } else {
                         hit = contains(P.nbr, s_gb, s_ge, x, words);
                     }
-                    if (hit) atomicAdd(&S.tacc[src], 1u);
+                    if (hit) atomicAdd(&AUXW(3, src), 1u);
                 }
             }
             __syncwarp();
-            ar = S.tacc[lane];
+            ar = AUXW(3, lane);
         }
         if (F) cnt -= ar - inAR;
     }
@@ -1327,8 +1368,8 @@ template <int D>
 __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, uint32_t lane, uint32_t *dst) {
     uint32_t p = lane;
     for (int i = level; i >= 0; --i) {
-        dst[i] = S.v[i][p];
-        p = S.pid[i][p];
+        dst[i] = S.lv[i].v[p];
+        p = S.lv[i].pid[p];
     }
 }
 
@@ -1349,12 +1390,12 @@ __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, ui
 // never runs, and the instruction-cache misses it causes cost 14-18 % on the rmat18 dense
 // queries (the pair-counting split).
 template <int D, bool ENUM, bool WORDS, int MODE>
-__global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
+__global__ void __launch_bounds__(dfs_max_warps<D>() * 32, GM_DFS_MINB_D(D)) k_dfs(const SearchParams P) {
     constexpr bool SIB = MODE == kModePat;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t *wbase = smem_raw + (size_t)(threadIdx.x >> 5) * P.warp_stride;
     WarpStack<D> &S = *reinterpret_cast<WarpStack<D> *>(wbase);
-    uint32_t *__restrict__ scr = reinterpret_cast<uint32_t *>(wbase + sizeof(WarpStack<D>));
+    uint32_t *__restrict__ scr = reinterpret_cast<uint32_t *>(wbase + P.stack_bytes);
     const uint32_t lane = threadIdx.x & 31;
     const int last = (int)P.nq - 1;
     // this warp's sibling buffer (32 parent lanes x sib_cap words)
@@ -1437,8 +1478,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 const bool valid = lane < k;
                 const int d0 = (int)P.d0;
                 for (int i = 0; i < d0; ++i) {
-                    S.v[i][lane] = valid ? P.pool[(unsigned long long)i * P.pool_size + b + lane] : 0;
-                    S.pid[i][lane] = (uint8_t)lane;
+                    S.lv[i].v[lane] = valid ? P.pool[(unsigned long long)i * P.pool_size + b + lane] : 0;
+                    S.lv[i].pid[lane] = (uint8_t)lane;
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
@@ -1462,10 +1503,9 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 const volatile uint32_t *it =
                     (GM_TEAMN(P) ? P.team_items[src_rank] : P.q_items) + slot * kItemWords;
                 const uint32_t depth = it[0];
-                if (lane < depth) { S.v[lane][0] = it[6 + lane]; S.pid[lane][0] = 0; }
-                S.cb[depth][lane] = lane == 0 ? it[1] : 0;
-                S.cl[depth][lane] = lane == 0 ? it[2] : 0;
-                S.cs[depth][lane] = (uint8_t)(lane == 0 ? it[3] : 0);
+                if (lane < depth) { S.lv[lane].v[0] = it[6 + lane]; S.lv[lane].pid[0] = 0; }
+                S.lv[depth].cb[lane] = lane == 0 ? it[1] : 0;
+                S.lv[depth].set(lane, lane == 0 ? it[2] : 0u, lane == 0 ? it[3] : 0u);
                 if (lane == 0) S.home = it[4];
                 __syncwarp();
                 if (lane == 0) {   // release the slot for the next lap of the ring
@@ -1517,7 +1557,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     for (int s = base; s <= top && !served; ++s) {
                         const uint32_t ci = S.ci[s], cj = S.cj[s];
                         if (ci >= 32) continue;
-                        const uint32_t cl = S.cl[s][lane];
+                        const uint32_t cl = S.lv[s].len(lane);
                         // worth a hand-off: >= 2 levels left below s, or >= 256 untouched tasks
                         const uint32_t myrem = lane > ci ? cl : (lane == ci ? cl - cj : 0u);
                         const uint32_t remtot = __reduce_add_sync(FULL, min(myrem, 1u << 20));
@@ -1528,7 +1568,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                             giver = 31 - __clz(mask);
                             give = __shfl_sync(FULL, cl, giver);
                         } else {
-                            const uint32_t rem = S.cl[s][ci] - cj;
+                            const uint32_t rem = S.lv[s].len(ci) - cj;
                             if (rem >= 2) { giver = ci; keep = rem / 2; give = rem - keep; gb = cj + keep; }
                         }
                         if (giver == 32) continue;
@@ -1558,10 +1598,10 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         if (pos == ~0ull) break;          // ring full: keep the work
                         if (lane == giver) {
                             uint32_t *it = P.q_items + (pos % P.q_cap) * kItemWords;
-                            it[0] = (uint32_t)s; it[1] = S.cb[s][giver] + gb; it[2] = give; it[3] = S.cs[s][giver];
+                            it[0] = (uint32_t)s; it[1] = S.lv[s].cb[giver] + gb; it[2] = give; it[3] = S.lv[s].src(giver);
                             it[4] = S.home; it[5] = P.epoch;
                             read_prefix<D>(S, s - 1, giver, it + 6);
-                            S.cl[s][giver] = mask ? 0u : gb;
+                            S.lv[s].set_len(giver, mask ? 0u : gb);
                             if (GM_TEAMN(P)) __threadfence_system(); else __threadfence();
                             ((volatile unsigned long long *)P.q_seq)[pos % P.q_cap] = pos + 1;
                         }
@@ -1587,7 +1627,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 constexpr int WT = D > 16 ? GM_WIDE_T32 : (D > 8 ? GM_WIDE_T16 : (SIB ? GM_WIDE_TSIB : GM_WIDE_T));
                 const uint32_t ci = S.ci[l], cj = S.cj[l];
                 uint32_t tsrc[WT], toff[WT], k;
-                const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
+                const uint32_t cl_ci = ci < 32 ? S.lv[l].len(ci) : 0u;
                 if (ci < 32 && cl_ci - cj >= 32u * WT) {
 #pragma unroll
                     for (int t = 0; t < WT; ++t) { tsrc[t] = ci; toff[t] = cj + 32u * t + lane; }
@@ -1598,7 +1638,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                     }
                 } else {
                     uint32_t rem = 0;
-                    if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
+                    if (lane >= ci) rem = S.lv[l].len(lane) - (lane == ci ? cj : 0);
                     const uint32_t rw = min(rem, 32u * WT);
                     uint32_t incl = rw;
 #pragma unroll
@@ -1633,7 +1673,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                         if (lj == (uint32_t)t) { ls = tsrc[t]; lo = toff[t]; }
                     const uint32_t lsrc = __shfl_sync(FULL, ls, lt), loff = __shfl_sync(FULL, lo, lt);
                     if (lane == 0) {
-                        if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
+                        if (loff + 1 < S.lv[l].len(lsrc)) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
                         else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
                     }
                 }
@@ -1708,7 +1748,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
             // ---- ScatterTask, warp-parallel: next 32 tasks of the virtual task pool at level l
             const uint32_t ci = S.ci[l], cj = S.cj[l];
             uint32_t src, off, k;
-            const uint32_t cl_ci = ci < 32 ? S.cl[l][ci] : 0u;
+            const uint32_t cl_ci = ci < 32 ? S.lv[l].len(ci) : 0u;
             if (cl_ci - cj >= 32 && ci < 32) {
                 // fast path: the cursor's slice alone fills the batch (long slices, hubs)
                 src = ci; off = cj + lane; k = 32;
@@ -1718,7 +1758,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 }
             } else {
                 uint32_t rem = 0;
-                if (lane >= ci) rem = S.cl[l][lane] - (lane == ci ? cj : 0);
+                if (lane >= ci) rem = S.lv[l].len(lane) - (lane == ci ? cj : 0);
                 const uint32_t r32 = min(rem, 32u);
                 uint32_t incl = r32;
 #pragma unroll
@@ -1742,7 +1782,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 const uint32_t lsrc = __shfl_sync(FULL, src, k - 1);
                 const uint32_t loff = __shfl_sync(FULL, off, k - 1);
                 if (lane == 0) {
-                    if (loff + 1 < S.cl[l][lsrc]) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
+                    if (loff + 1 < S.lv[l].len(lsrc)) { S.ci[l] = lsrc; S.cj[l] = loff + 1; }
                     else { S.ci[l] = lsrc + 1; S.cj[l] = 0; }
                 }
             }
@@ -1785,8 +1825,8 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                             row[P.col[l]] = ld_nc(P.new2old + v);        // original ids out
                             uint32_t p = src;
                             for (int i = l - 1; i >= 0; --i) {
-                                row[P.col[i]] = ld_nc(P.new2old + S.v[i][p]);
-                                p = S.pid[i][p];
+                                row[P.col[i]] = ld_nc(P.new2old + S.lv[i].v[p]);
+                                p = S.lv[i].pid[p];
                             }
                         }
                     }
@@ -1802,7 +1842,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 __syncwarp();
                 continue;
             }
-            if (has) { S.v[l][lane] = v; S.pid[l][lane] = (uint8_t)src; }
+            if (has) { S.lv[l].v[lane] = v; S.lv[l].pid[lane] = (uint8_t)src; }
             const uint32_t fm = __ballot_sync(FULL, F);
             __syncwarp();
             if (!fm) continue;
@@ -1813,8 +1853,7 @@ __global__ void __launch_bounds__(kDfsMaxWarps * 32, GM_DFS_MINB_D(D)) k_dfs(con
                 const bool sibok = F && pos < P.sib_cap;
                 generate<D>(P, S, l + 1, F && !sibok, lane, wacc);
                 if (sibok) {
-                    S.cb[l + 1][lane] = sib_base + src * P.sib_cap; S.cl[l + 1][lane] = pos;
-                    S.cs[l + 1][lane] = kSibCs;
+                    S.lv[l + 1].cb[lane] = sib_base + src * P.sib_cap; S.lv[l + 1].set(lane, pos, kSibCs);
                 }
             } else if (GM_GEN_CACHE && SIB && l + 1 == (int)P.gen_level) {
                 generate_cached<D>(P, S, scr, l + 1, F, lane, wacc);
@@ -2044,21 +2083,51 @@ static int ensure(uint32_t *&p, size_t &have, size_t need) {
     return GM_OK;
 }
 
+// shared memory of a warp's stack with `levels` levels allocated
 template <int D>
-static size_t stack_bytes() { return sizeof(WarpStack<D>); }
+static size_t stack_bytes(uint32_t levels) { return offsetof(WarpStack<D>, lv) + sizeof(StackLevel) * levels; }
 
 template <int D, bool ENUM, bool WORDS, int MODE>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
                       uint32_t *grid_out, uint32_t *block_out) {
-    P.warp_stride = (uint32_t)(stack_bytes<D>() + 128ull * (P.rows_chk + P.rows_last + P.rows_gen));
-    const size_t smem = (size_t)P.warp_stride * wpb;
+    // levels: at most D (a query of nq <= D vertices, its counted last levels not stored)
+    P.levels = std::min<uint32_t>(P.levels ? P.levels : (uint32_t)D, (uint32_t)D);
+    P.stack_bytes = (uint32_t)stack_bytes<D>(P.levels);
+    P.aux_row = P.rows_chk + P.rows_last + P.rows_gen;
+    P.warp_stride = (uint32_t)(P.stack_bytes + 128ull * (P.aux_row + P.rows_aux));
     auto kern = k_dfs<D, ENUM, WORDS, MODE>;
-    GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int fit = 0;
-    GM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, (int)(wpb * 32), smem));
+    constexpr uint32_t wmax = dfs_max_warps<D>();
+    GM_REQ(wpb <= wmax, GM_ERR_ARG, "warps_per_block %u > %u (k_dfs<%d> launch bounds)", wpb, wmax, D);
+    GM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::min<size_t>((size_t)P.warp_stride * (wpb ? wpb : wmax), 227u * 1024u)));
+    // resident blocks for w warps per block (0 when a block does not fit)
+    auto fit_for = [&](uint32_t w) -> int {
+        if ((size_t)P.warp_stride * w > 227u * 1024u) return 0;
+        int f = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f, kern, (int)(w * 32), (size_t)P.warp_stride * w) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return f;
+    };
+    if (!wpb) {   // the block size with the most resident warps (ties: the larger block)
+        uint32_t best = 0;
+        for (uint32_t w = 1; w <= wmax; ++w) {
+            const int f = fit_for(w);
+            if (f > 0 && (uint32_t)f * w >= best) { best = (uint32_t)f * w; wpb = w; }
+        }
+        GM_REQ(best > 0, GM_ERR_LIMIT, "k_dfs: no block fits (%u B of shared memory per warp)", P.warp_stride);
+    }
+    const size_t smem = (size_t)P.warp_stride * wpb;
+    const int fit = fit_for(wpb);
     GM_REQ(fit > 0, GM_ERR_LIMIT, "k_dfs: no block fits (smem %zu)", smem);
     const int per = bps ? std::min<int>((int)bps, fit) : fit;
     const uint32_t grid = (uint32_t)(sms * per);
+    static const bool dbg = getenv("GM_DEBUG_LAUNCH") != nullptr;
+    if (dbg)
+        fprintf(stderr, "[gm] k_dfs<%d,%d,%d,%d> stack %zu B + %u scratch rows = %u B/warp, %u warps/block, "
+                "%d blocks/SM fit, %d launched\n", D, (int)ENUM, (int)WORDS, MODE, (size_t)P.stack_bytes,
+                P.aux_row + P.rows_aux, P.warp_stride, wpb, fit, per);
     // pool items per fetch: 32 (a full warp of parent lanes) when the pool is large; fewer
     // when it is small, so that every warp gets some initial work (§4.3).
     const unsigned long long nwarps = (unsigned long long)grid * wpb;
@@ -2128,7 +2197,7 @@ extern "C" void gm_default_opts(gm_run_opts *o) {
     o->world = 1;
     o->root_chunk = 64;
     o->steal = 1;
-    o->warps_per_block = 4;
+    o->warps_per_block = 0;       // per query: the most resident warps
     o->pool_bytes_max = 1ull << 30;
 }
 
@@ -2153,7 +2222,6 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         if (!o.tau) o.tau = 1000000;
         if (!o.world) o.world = 1;
         if (!o.root_chunk) o.root_chunk = 64;
-        if (!o.warps_per_block) o.warps_per_block = 4;
         if (!o.pool_bytes_max) o.pool_bytes_max = 1ull << 30;
     }
     GM_REQ(o.rank < o.world, GM_ERR_ARG, "rank %u >= world %u", o.rank, o.world);
@@ -2194,6 +2262,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     const bool use_sb = !enumerate && p->sb_ok && p->aut > 1 && !(o.flags & GM_FLAG_NO_SYMMETRY) && !o.roots;
     rs.automorphisms = use_sb ? p->aut : 1;
 
+    // a stack level packs a slice length with its source level (GM_PACK_CS): lengths < 2^27
+    GM_REQ(!GM_PACK_CS || g->dmax < (1u << 27), GM_ERR_LIMIT,
+           "k_dfs: a vertex of degree %u (stack slices hold lengths < 2^27)", g->dmax);
     SearchParams P;
     memset(&P, 0, sizeof(P));
     P.offs = g->offs; P.nbr = g->nbr; P.cand = p->cand;
@@ -2501,8 +2572,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
                     }
                 }
                 if (ok) {
-                    // one buffer row set per warp a grid can hold (<= 16 blocks of kDfsMaxWarps per SM)
-                    const size_t need = sizeof(uint32_t) * (size_t)W.sms * 16 * kDfsMaxWarps * 32 * kSibCap;
+                    // one buffer row set per warp a grid can hold (8-level kernels: <= 16 blocks of
+                    // 4 warps per SM)
+                    const size_t need = sizeof(uint32_t) * (size_t)W.sms * 16 * dfs_max_warps<8>() * 32 * kSibCap;
                     rc = ensure(W.sib, W.sib_bytes, need);
                     if (rc) return rc;
                     P.sib = W.sib;
@@ -2567,6 +2639,19 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
         // level by tasks: no counting code)
         const int mode = (nq <= 8 && (P.sib_level || P.gen_level)) ? kModePat
                        : (P.bulk_two ? kModePair : (P.bulk_last ? kModeSet : kModePlain));
+        {   // stack levels the search touches: the slice of level `top` is the deepest entry
+            // written (a counted level -- set counting of the last, pair counting of the last
+            // two -- is never entered; only the flags the launched kernel honours count)
+            const bool eff_two = !enumerate && mode == kModePair && P.bulk_two;
+            const bool eff_last = !enumerate && (mode == kModeSet || mode == kModePair) && P.bulk_last;
+            const uint32_t last = nq - 1;
+            uint32_t top = last;
+            if (eff_two && P.d0 + 2 <= last) top = last - 2;
+            else if (eff_last && P.d0 + 1 <= last) top = last - 1;
+            P.levels = top + 1;
+            // counting state rows: the kernels of these modes run prep_last / prep_two
+            P.rows_aux = enumerate ? 0u : (mode == kModePair ? 4u : (mode == kModeSet ? 3u : 0u));
+        }
         if (enumerate)   // (enumerate never counts words: its cost is the output)
             rc = nq <= 8 ? GM_LAUNCH(8, true, false, kModePlain)
                          : (nq <= 16 ? GM_LAUNCH(16, true, false, kModePlain) : GM_LAUNCH(32, true, false, kModePlain));

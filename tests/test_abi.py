@@ -43,7 +43,7 @@ def test_default_opts_layout():
     o = _lib.RunOpts()
     _lib.lib().gm_default_opts(ctypes.byref(o))
     assert o.tau == 1000000 and o.world == 1 and o.root_chunk == 64 and o.steal == 1
-    assert o.warps_per_block == 4 and o.pool_bytes_max == 1 << 30
+    assert o.warps_per_block == 0 and o.pool_bytes_max == 1 << 30   # 0: per query, the most resident warps
     # struct sizes match the C layout (checked with a tiny C program compiled by gcc)
     src = r'''
     #include <stdio.h>

@@ -122,6 +122,33 @@ def test_dense_query_counts_and_sets(env, k, seed):
     check_all_paths(env, q)
 
 
+@pytest.mark.parametrize("k,seed,leaves,same", [(12, 1, 0, False), (14, 3, 1, False), (14, 1, 2, True),
+                                                 (22, 1, 2, False), (30, 2, 1, False), (32, 1, 0, False)])
+def test_block_shapes_deep_kernels(env, k, seed, leaves, same):
+    """The 16/24/32-level kernels are compiled for blocks of up to 14 warps; the default picks
+    the block size with the most resident warps for the query's shared memory (stack levels
+    the query touches + scratch rows).  Every explicit block size, with stealing and a small
+    pool (many warps share few items), gives the oracle's count; 15 warps is an argument error."""
+    gm = env["gm"]
+    q = query(env, k, seed, leaves, same)
+    ref = oracle_count(env, q)
+    p = gm.gm_plan_query(env["g"], q)
+    c, st = gm.gm_count(p, tau=1)
+    assert c == ref and st["dfs_launches"] and st["block"] % 32 == 0 and 32 <= st["block"] <= 14 * 32, st
+    for wpb in (1, 3, 5, 7, 14):
+        for bps in (0, 1):
+            try:
+                c, st = gm.gm_count(p, tau=64, warps_per_block=wpb, blocks_per_sm=bps)
+            except gm.GMError as e:      # a block of wpb warps larger than 227 KB of shared memory
+                assert wpb >= 7 and "no block fits" in str(e), (q.name, wpb, e)
+                continue
+            assert c == ref, (q.name, wpb, bps, st)
+            if st["dfs_launches"]:
+                assert st["block"] == 32 * wpb
+    with pytest.raises(gm.GMError):
+        gm.gm_count(p, warps_per_block=15)
+
+
 @pytest.mark.parametrize("k,seed,leaves,same", LEAVES)
 def test_dense_core_with_leaves(env, k, seed, leaves, same):
     """Dense cores plus one or two pendant leaves, in the planner's order and with the leaves

@@ -663,7 +663,8 @@ def test_pool_depth_sweep_counting_paths(gm, seed):
 
 def test_launch_shape_options(gm):
     """warps_per_block 1/2/4 and blocks_per_sm give the oracle's count; more warps per block
-    than k_dfs is compiled for is an argument error, not a failed launch."""
+    than k_dfs is compiled for (4 for the 8-level kernels, 14 for the deeper ones) is an
+    argument error, not a failed launch."""
     n, s, d = gi.rmat_edges(9, 8, 5)
     lab = gi.uniform_labels(n, 2, 5)
     q = small_random_query(5, 5, 2)
@@ -672,9 +673,10 @@ def test_launch_shape_options(gm):
     for wpb in (1, 2, 4):
         for bps in (0, 1, 3):
             assert gm.gm_count(p, warps_per_block=wpb, blocks_per_sm=bps, tau=16)[0] == ref
-    with pytest.raises(gm.GMError) as e:
-        gm.gm_count(p, warps_per_block=8)
-    assert "warps_per_block" in str(e.value)
+    for wpb in (8, 15):
+        with pytest.raises(gm.GMError) as e:
+            gm.gm_count(p, warps_per_block=wpb, tau=16)
+        assert "warps_per_block" in str(e.value)
 
 
 def test_pair_count_long_lists_closed_form(gm):
