@@ -26,8 +26,9 @@
  *   - Vertex ids are uint32 in [0, n); labels are uint32 in [0, num_labels).
  *   - Limits: n * num_labels < 2^32, stored adjacency entries < 2^32,
  *     query size 1 <= nq <= GM_MAX_QUERY, and (gm_count / gm_enumerate) maximum degree
- *     < 2^27 (a DFS stack entry packs a slice length with its source level).
- *     Exceeding a limit returns GM_ERR_LIMIT.
+ *     < 2^27 and, for queries of more than 8 vertices, n < 2^27 (a DFS stack entry packs a
+ *     slice length with its source level, and a vertex id with its parent lane; DESIGN.md
+ *     §5).  Exceeding a limit returns GM_ERR_LIMIT.
  */
 #ifndef GMATCH_H
 #define GMATCH_H

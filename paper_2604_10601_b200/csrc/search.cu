@@ -147,6 +147,9 @@ constexpr uint32_t kStageWords = 256;          // staging buffer: 8 scratch rows
 #define GM_TEAM_CODE 1     // (A/B switch) 0 compiles the cross-GPU stealing team code out of the kernels
 #endif
 #define GM_TEAMN(P) (GM_TEAM_CODE ? (P).team_n : 0u)
+#ifndef GM_PACK_PID
+#define GM_PACK_PID 1      // 16/24/32-level kernels: the parent lane in the top 5 bits of the vertex word
+#endif
 #ifndef GM_PACK_CS
 #define GM_PACK_CS 1       // the slice's source level in the top 5 bits of its length (416-byte levels)
 #endif
@@ -453,11 +456,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// One level l of a warp's DFS stack (§4.2, Alg. 2 S[l][lane]): 448 bytes, or 416 with the
-// slice length and source level packed in one word (GM_PACK_CS: lengths < 2^27, a row
-// bound gm_count checks; source levels < 31, and 31 marks a sibling-buffer slice).
-struct alignas(16) StackLevel {
-    uint32_t v[32];       // S[l][lane].v   : candidate data vertex of the task in this lane
+// One level l of a warp's DFS stack (§4.2, Alg. 2 S[l][lane]).  448 bytes; 416 with the
+// slice length and source level packed in one word (GM_PACK_CS: lengths < 2^27, a degree
+// bound gm_count checks; source levels < 31, and 31 marks a sibling-buffer slice); 384 when
+// also the parent lane rides in the top 5 bits of the vertex word (PK: the 16/24/32-level
+// kernels with GM_PACK_PID, vertex ids < 2^27, checked by gm_count).
+template <bool PK>
+struct StackPid { uint8_t pid[32]; };   // S[l][lane].pid : parent lane at level l-1
+template <>
+struct StackPid<true> {};
+template <bool PK>
+struct alignas(16) StackLevel : StackPid<PK> {
+    uint32_t v[32];       // S[l][lane].v   : candidate data vertex of the task in this lane (PK: | pid << 27)
     uint32_t cb[32];      // S[l][lane].C   : begin of the local candidate slice of lane's partial match
 #if GM_PACK_CS
     uint32_t clcs[32];    //                  its length | (source level << 27)
@@ -465,13 +475,21 @@ struct alignas(16) StackLevel {
     uint32_t cl[32];      //                  its length
     uint8_t cs[32];       //                  level whose vertex produced the slice (its check is implied)
 #endif
-    uint8_t pid[32];      // S[l][lane].pid : parent lane at level l-1
+    static constexpr uint32_t kLow27 = (1u << 27) - 1;
+    __device__ __forceinline__ uint32_t vtx(uint32_t j) const {
+        if constexpr (PK) return v[j] & kLow27; else return v[j];
+    }
+    __device__ __forceinline__ uint32_t par(uint32_t j) const {
+        if constexpr (PK) return v[j] >> 27; else return this->pid[j];
+    }
+    __device__ __forceinline__ void set_vp(uint32_t j, uint32_t x, uint32_t p) {
+        if constexpr (PK) v[j] = x | (p << 27); else { v[j] = x; this->pid[j] = (uint8_t)p; }
+    }
 #if GM_PACK_CS
-    static constexpr uint32_t kClMask = (1u << 27) - 1;
-    __device__ __forceinline__ uint32_t len(uint32_t j) const { return clcs[j] & kClMask; }
+    __device__ __forceinline__ uint32_t len(uint32_t j) const { return clcs[j] & kLow27; }
     __device__ __forceinline__ uint32_t src(uint32_t j) const { return clcs[j] >> 27; }
     __device__ __forceinline__ void set(uint32_t j, uint32_t n, uint32_t s) { clcs[j] = n | (s << 27); }
-    __device__ __forceinline__ void set_len(uint32_t j, uint32_t n) { clcs[j] = (clcs[j] & ~kClMask) | n; }
+    __device__ __forceinline__ void set_len(uint32_t j, uint32_t n) { clcs[j] = (clcs[j] & ~kLow27) | n; }
 #else
     __device__ __forceinline__ uint32_t len(uint32_t j) const { return cl[j]; }
     __device__ __forceinline__ uint32_t src(uint32_t j) const { return cs[j]; }
@@ -493,7 +511,8 @@ struct alignas(16) WarpStack {
     uint32_t sibn[D <= 8 ? 32 : 1];   // sibling prefixes (8-level kernels only): siblings per parent lane
     uint32_t ci[D];       // virtual-task-pool cursor: source lane ...
     uint32_t cj[D];       // ... and offset inside its slice (§4.2 "two lightweight pointers")
-    StackLevel lv[D];     // levels 0 .. SearchParams.levels - 1 are allocated
+    using Level = StackLevel<(D > 8 && GM_PACK_PID != 0)>;
+    Level lv[D];          // levels 0 .. SearchParams.levels - 1 are allocated
 };
 
 // GenerateTask (Alg. 2 lines 17-24, Erratum 2 read as a running minimum): the local
@@ -517,15 +536,15 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
             // row (a low-degree vertex's neighbours are mostly high-degree, i.e. small ids).
             // First the bounds, then each row's cut by two binary searches.
             for (int i = l - 1; i >= lowest; --i) {
-                const uint32_t w = S.lv[i].v[p];
+                const uint32_t w = S.lv[i].vtx(p);
                 if ((gt >> i) & 1u) lb = max(lb, w + 1);
                 if ((lt >> i) & 1u) ub = min(ub, w);
-                p = S.lv[i].pid[p];
+                p = S.lv[i].par(p);
             }
             p = lane;
             for (int i = l - 1; i >= lowest; --i) {
                 if ((bw >> i) & 1u) {
-                    const uint32_t row = S.lv[i].v[p] * P.S + lab;
+                    const uint32_t row = S.lv[i].vtx(p) * P.S + lab;
                     const uint32_t lo = ld_nc(P.offs + row), len = ld_nc(P.offs + row + 1) - lo;
                     words += 2;
                     if (lb < ub && len) {
@@ -536,11 +555,11 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
                         best = 0; cb = lo; cs = (uint32_t)i;
                     }
                 }
-                p = S.lv[i].pid[p];
+                p = S.lv[i].par(p);
             }
         } else {
             for (int i = l - 1; i >= lowest; --i) {
-                const uint32_t w = S.lv[i].v[p];
+                const uint32_t w = S.lv[i].vtx(p);
                 if ((bw >> i) & 1u) {
                     const uint32_t row = w * P.S + lab;
                     const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
@@ -549,7 +568,7 @@ __device__ __forceinline__ void generate(const SearchParams &P, WarpStack<D> &S,
                 }
                 if ((gt >> i) & 1u) lb = max(lb, w + 1);
                 if ((lt >> i) & 1u) ub = min(ub, w);
-                p = S.lv[i].pid[p];
+                p = S.lv[i].par(p);
             }
             if (gt | lt) {   // the slice is sorted: cut it to the ids the conditions allow
                 uint32_t a = 0, e = best;
@@ -586,7 +605,7 @@ __device__ __forceinline__ void gen_prep(const SearchParams &P, WarpStack<D> &S,
     const int lowest = __ffs(bw | gt | lt) - 1;
     uint32_t p = lane;
     for (int i = l - 2; i >= lowest && lowest >= 0; --i) {
-        const uint32_t w = S.lv[i].v[p];
+        const uint32_t w = S.lv[i].vtx(p);
         if ((bw >> i) & 1u) {
             const uint32_t row = w * P.S + lab;
             const uint32_t lo = ld_nc(P.offs + row), hi = ld_nc(P.offs + row + 1);
@@ -595,7 +614,7 @@ __device__ __forceinline__ void gen_prep(const SearchParams &P, WarpStack<D> &S,
         }
         if ((gt >> i) & 1u) lb = max(lb, w + 1);
         if ((lt >> i) & 1u) ub = min(ub, w);
-        p = S.lv[i].pid[p];
+        p = S.lv[i].par(p);
     }
     if (bw && (gt | lt)) {
         uint32_t a = 0, e = best;
@@ -612,8 +631,8 @@ __device__ __forceinline__ void generate_cached(const SearchParams &P, WarpStack
                                                 bool valid, uint32_t lane, uint32_t &words) {
     uint32_t best = 0, cb = 0, cs = 0;
     if (valid) {
-        const uint32_t p = S.lv[l - 1].pid[lane];
-        const uint32_t v1 = S.lv[l - 1].v[lane];
+        const uint32_t p = S.lv[l - 1].par(lane);
+        const uint32_t v1 = S.lv[l - 1].vtx(lane);
         const uint32_t nb = (P.bw[l] >> (l - 1)) & 1u;
         const uint32_t ngt = (P.sb_gt[l] >> (l - 1)) & 1u, nlt = (P.sb_lt[l] >> (l - 1)) & 1u;
         cb = GENW(0, p); best = GENW(1, p); cs = GENW(2, p);
@@ -688,12 +707,12 @@ __device__ __forceinline__ bool process(const SearchParams &P, WarpStack<D> &S, 
         // (ordering hub checks first measured 1-7 % slower on rmat18 dense queries: pairs of
         // mixed hub/search probes overlap better)
         for (int i = l - 1; i >= (int)P.walk_low[l]; --i) {   // injectivity + collect the checks
-            const uint32_t w = S.lv[i].v[p];
+            const uint32_t w = S.lv[i].vtx(p);
             if ((eq >> i) & 1u) ok = ok && (w != v);
             if ((gt >> i) & 1u) ok = ok && (v > w);            // symmetry-breaking conditions
             if ((lt >> i) & 1u) ok = ok && (v < w);
             if ((chk >> i) & 1u) { CHK(k, lane) = w; ++k; }
-            p = S.lv[i].pid[p];
+            p = S.lv[i].par(p);
         }
     }
     ok = ok && ((cword >> (v & 31)) & 1u);          // filter verdict gates the probes below
@@ -880,10 +899,10 @@ __device__ __forceinline__ void prep_checks(const SearchParams &P, WarpStack<D> 
     int kc = 0, ke = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.par_low; --i) {
-        const uint32_t w = S.lv[i].v[p];
+        const uint32_t w = S.lv[i].vtx(p);
         if ((chkm >> i) & 1u) { CHK(kc, lane) = w; ++kc; }
         if ((eqm >> i) & 1u) { CHK(nchk + ke, lane) = w; ++ke; }
-        p = S.lv[i].pid[p];
+        p = S.lv[i].par(p);
     }
     if (SIB && P.sib_level) {
         for (int k = kc; k < nchk; ++k) CHK(k, lane) = ~0u;
@@ -966,13 +985,13 @@ __device__ __forceinline__ void prep_last(const SearchParams &P, WarpStack<D> &S
     int k = 0, ka = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.last_low; --i) {
-        const uint32_t w = S.lv[i].v[p];
+        const uint32_t w = S.lv[i].vtx(p);
         if (i == b) mb = w;
         if ((test >> i) & 1u) { LASTW(k, lane) = w; ++k; }
         if ((known >> i) & 1u) { LASTW(P.last_k + ka, lane) = w; ++ka; }
         if ((gt >> i) & 1u) lb = max(lb, w + 1);
         if ((lt >> i) & 1u) ub = min(ub, w);
-        p = S.lv[i].pid[p];
+        p = S.lv[i].par(p);
     }
     AUXW(0, lane) = mb;
     AUXW(1, lane) = lb;
@@ -1051,10 +1070,10 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
     uint32_t m6 = 0, m7 = 0;
     uint32_t p = lane;
     for (int i = l - 1; i >= (int)P.two_low; --i) {
-        const uint32_t w = S.lv[i].v[p];
+        const uint32_t w = S.lv[i].vtx(p);
         if (i == b6) m6 = w;
         if (i == b7) m7 = w;
-        p = S.lv[i].pid[p];
+        p = S.lv[i].par(p);
     }
     LASTW(0, lane) = m6;
     LASTW(1, lane) = m7;
@@ -1072,12 +1091,12 @@ __device__ __forceinline__ void prep_two(const SearchParams &P, WarpStack<D> &S,
     if (!P.two_walk) {
         p = lane;
         for (int i = l - 1; i >= (int)P.two_low; --i) {
-            const uint32_t w = S.lv[i].v[p];
+            const uint32_t w = S.lv[i].vtx(p);
             bool a = false, r = false;
             if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], w, lab6, words);
             if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], w, lab7, words);
             inA += a; inR += r; inAR += a && r;
-            p = S.lv[i].pid[p];
+            p = S.lv[i].par(p);
         }
     }
     AUXW(0, lane) = inA;
@@ -1118,12 +1137,12 @@ __device__ __forceinline__ unsigned long long count_two(const SearchParams &P, W
         if (P.two_walk) {       // a per-task row with same-label images below l: test them all here
             uint32_t p = src;
             for (int i = l - 1; i >= (int)P.two_low; --i) {
-                const uint32_t w = S.lv[i].v[p];
+                const uint32_t w = S.lv[i].vtx(p);
                 bool a = false, r = false;
                 if ((P.two_same6 >> i) & 1u) a = ((P.two_adj6 >> i) & 1u) || has_edge<(D > 8)>(P, m6, P.lab[b6], w, lab6, words);
                 if ((P.two_same7 >> i) & 1u) r = ((P.two_adj7 >> i) & 1u) || has_edge<(D > 8)>(P, m7, P.lab[b7], w, lab7, words);
                 inA += a; inR += r; inAR += a && r;
-                p = S.lv[i].pid[p];
+                p = S.lv[i].par(p);
             }
         } else {                // every image below l was tested once per parent
             inA = AUXW(0, src); inR = AUXW(1, src); inAR = AUXW(2, src);
@@ -1368,8 +1387,8 @@ template <int D>
 __device__ __forceinline__ void read_prefix(const WarpStack<D> &S, int level, uint32_t lane, uint32_t *dst) {
     uint32_t p = lane;
     for (int i = level; i >= 0; --i) {
-        dst[i] = S.lv[i].v[p];
-        p = S.lv[i].pid[p];
+        dst[i] = S.lv[i].vtx(p);
+        p = S.lv[i].par(p);
     }
 }
 
@@ -1478,8 +1497,7 @@ __global__ void __launch_bounds__(dfs_max_warps<D>() * 32, GM_DFS_MINB_D(D)) k_d
                 const bool valid = lane < k;
                 const int d0 = (int)P.d0;
                 for (int i = 0; i < d0; ++i) {
-                    S.lv[i].v[lane] = valid ? P.pool[(unsigned long long)i * P.pool_size + b + lane] : 0;
-                    S.lv[i].pid[lane] = (uint8_t)lane;
+                    S.lv[i].set_vp(lane, valid ? P.pool[(unsigned long long)i * P.pool_size + b + lane] : 0u, lane);
                 }
                 __syncwarp();
                 generate<D>(P, S, d0, valid, lane, wacc);
@@ -1503,7 +1521,7 @@ __global__ void __launch_bounds__(dfs_max_warps<D>() * 32, GM_DFS_MINB_D(D)) k_d
                 const volatile uint32_t *it =
                     (GM_TEAMN(P) ? P.team_items[src_rank] : P.q_items) + slot * kItemWords;
                 const uint32_t depth = it[0];
-                if (lane < depth) { S.lv[lane].v[0] = it[6 + lane]; S.lv[lane].pid[0] = 0; }
+                if (lane < depth) S.lv[lane].set_vp(0, it[6 + lane], 0);
                 S.lv[depth].cb[lane] = lane == 0 ? it[1] : 0;
                 S.lv[depth].set(lane, lane == 0 ? it[2] : 0u, lane == 0 ? it[3] : 0u);
                 if (lane == 0) S.home = it[4];
@@ -1825,8 +1843,8 @@ __global__ void __launch_bounds__(dfs_max_warps<D>() * 32, GM_DFS_MINB_D(D)) k_d
                             row[P.col[l]] = ld_nc(P.new2old + v);        // original ids out
                             uint32_t p = src;
                             for (int i = l - 1; i >= 0; --i) {
-                                row[P.col[i]] = ld_nc(P.new2old + S.lv[i].v[p]);
-                                p = S.lv[i].pid[p];
+                                row[P.col[i]] = ld_nc(P.new2old + S.lv[i].vtx(p));
+                                p = S.lv[i].par(p);
                             }
                         }
                     }
@@ -1842,7 +1860,7 @@ __global__ void __launch_bounds__(dfs_max_warps<D>() * 32, GM_DFS_MINB_D(D)) k_d
                 __syncwarp();
                 continue;
             }
-            if (has) { S.lv[l].v[lane] = v; S.lv[l].pid[lane] = (uint8_t)src; }
+            if (has) S.lv[l].set_vp(lane, v, src);
             const uint32_t fm = __ballot_sync(FULL, F);
             __syncwarp();
             if (!fm) continue;
@@ -2085,7 +2103,12 @@ static int ensure(uint32_t *&p, size_t &have, size_t need) {
 
 // shared memory of a warp's stack with `levels` levels allocated
 template <int D>
-static size_t stack_bytes(uint32_t levels) { return offsetof(WarpStack<D>, lv) + sizeof(StackLevel) * levels; }
+static size_t stack_bytes(uint32_t levels) {
+    // lv is the last member and every Level is a multiple of 16 bytes: the header is the rest
+    using L = typename WarpStack<D>::Level;
+    static_assert(sizeof(L) % 16 == 0, "stack levels keep 16-byte alignment");
+    return sizeof(WarpStack<D>) - sizeof(L) * D + sizeof(L) * levels;
+}
 
 template <int D, bool ENUM, bool WORDS, int MODE>
 static int launch_dfs(SearchParams P, int sms, uint32_t wpb, uint32_t bps, uint32_t sharers, cudaStream_t st,
@@ -2265,6 +2288,9 @@ static int run_search(const gm_plan *p, const gm_run_opts *opts_in, bool enumera
     // a stack level packs a slice length with its source level (GM_PACK_CS): lengths < 2^27
     GM_REQ(!GM_PACK_CS || g->dmax < (1u << 27), GM_ERR_LIMIT,
            "k_dfs: a vertex of degree %u (stack slices hold lengths < 2^27)", g->dmax);
+    GM_REQ(!GM_PACK_PID || p->nq <= 8 || g->n < (1ull << 27), GM_ERR_LIMIT,
+           "k_dfs: %llu vertices (queries of > 8 vertices: stack entries hold vertex ids < 2^27)",
+           (unsigned long long)g->n);
     SearchParams P;
     memset(&P, 0, sizeof(P));
     P.offs = g->offs; P.nbr = g->nbr; P.cand = p->cand;
